@@ -1,0 +1,1140 @@
+// C ABI of the B200 PP-PC hot path (include/pppc_b200.h) and the host C++
+// PP-PC driver that mirrors solve_pp_pc (proj/src/engine.cpp:187-270).
+//
+// The context owns every device buffer (pattern, values, work vectors,
+// allocated once at ps_create); host arrays cross the ABI in the reference's
+// [count][dim] order and are transposed on the device into the interleaved
+// [dim][count] layout the kernels use.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "pppc_internal.h"
+
+using namespace pppc;
+
+namespace pppc {
+
+constexpr double kPi = 3.14159265358979323846;
+
+thread_local std::string g_global_error;
+
+struct Geometry {
+  int G = 0, C = 0, L = 0, Lp = 0, R = 0;
+  int* warp_row_begin = nullptr;
+};
+
+// Contiguous row ranges for C blocks x kWarps warps, balanced by row cost
+// (slots + vector streams).  Depends only on the pattern, C and R.
+int row_ranges(const std::vector<int>& h_rp, int C, int R, std::vector<int>* out) {
+  const int d = static_cast<int>(h_rp.size()) - 1;
+  const int parts = C * kWarps;
+  std::vector<double> cum(d + 1, 0.0);
+  for (int i = 0; i < d; ++i) cum[i + 1] = cum[i] + (h_rp[i + 1] - h_rp[i]) + 4.0;
+  out->assign(parts + 1, d);
+  (*out)[0] = 0;
+  int row = 0;
+  for (int k = 1; k < parts; ++k) {
+    const double goal = cum[d] * k / parts;
+    while (row < d && cum[row] < goal) ++row;
+    // keep ranges a multiple of R rows where possible (sub-row lanes)
+    int aligned = row - (row % R);
+    aligned = std::max(aligned, (*out)[k - 1]);
+    (*out)[k] = std::min(aligned, d);
+  }
+  (*out)[parts] = d;
+  return PS_OK;
+}
+
+}  // namespace pppc
+
+struct ps_ctx {
+  DevProblem P;
+  ps_time_mesh mesh{};
+  ps_solver_settings settings{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int max_batch = 0;
+  int capacity = 0;
+  // work buffers (interleaved, stride = batch count)
+  double *u = nullptr, *uprev = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
+  double *Dinv = nullptr, *A = nullptr;
+  double *io_a = nullptr, *io_b = nullptr;  // [count][d] staging
+  // kernel control
+  unsigned long long* sync = nullptr;
+  double* partials = nullptr;
+  size_t partials_len = 0;
+  int* abort_flag = nullptr;
+  SysOut* out = nullptr;
+  double* trace = nullptr;
+  int64_t* lockstep = nullptr;
+  double* coef = nullptr;
+  size_t coef_len = 0;
+  double* tnext = nullptr;
+  size_t tnext_len = 0;
+  std::map<int, Geometry> geo;
+  std::map<double, std::pair<double*, double*>> step_cache;  // dt -> (A, Dinv), linear_factor analogue
+  SpectralState* spec = nullptr;
+  int spec_N = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  std::mutex mu;
+};
+
+namespace {
+
+template <class T>
+bool dalloc(T** p, size_t n) {
+  if (n == 0) n = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)) == cudaSuccess;
+}
+
+struct Failure : std::runtime_error {
+  int code;
+  Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Failure(PS_ERR_CUDA, std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <class Fn>
+int guard(ps_ctx* ctx, Fn fn) {
+  try {
+    fn();
+    return PS_OK;
+  } catch (const Failure& f) {
+    if (ctx) ctx->err = f.what();
+    g_global_error = f.what();
+    return f.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    g_global_error = e.what();
+    return PS_ERR_BAD_ARG;
+  }
+}
+
+// TimeMesh (proj/include/parasteady/types.hpp:21-40)
+double coarse_dt(const ps_time_mesh& m) { return m.period / m.subintervals; }
+double fine_dt(const ps_time_mesh& m) { return coarse_dt(m) / m.fine_steps; }
+double boundary(const ps_time_mesh& m, int n) {
+  if (n == m.subintervals) return m.period;
+  return static_cast<double>(n) * m.period / m.subintervals;
+}
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw Failure(PS_ERR_CUDA, "cuda: no CUDA device available (the B200 path has no CPU fallback)");
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) throw Failure(PS_ERR_CUDA, "cuda: this library is built for sm_100a (B200) only");
+}
+
+void validate_desc(const ps_problem_desc* d) {
+  if (!d) throw Failure(PS_ERR_BAD_ARG, "problem: null description");
+  if (d->dim < 1) throw Failure(PS_ERR_BAD_ARG, "problem: excitation dimension must be positive");
+  if (!d->row_ptr || !d->col_idx || !d->mass) throw Failure(PS_ERR_BAD_ARG, "problem: missing CSR arrays");
+  if (d->row_ptr[0] != 0 || d->row_ptr[d->dim] != d->nnz) throw Failure(PS_ERR_BAD_ARG, "problem: bad row_ptr");
+  for (int i = 0; i < d->dim; ++i) {
+    if (d->row_ptr[i + 1] < d->row_ptr[i]) throw Failure(PS_ERR_BAD_ARG, "problem: bad row_ptr");
+    bool diag = false;
+    for (int k = d->row_ptr[i]; k < d->row_ptr[i + 1]; ++k) {
+      if (d->col_idx[k] < 0 || d->col_idx[k] >= d->dim) throw Failure(PS_ERR_BAD_ARG, "problem: column out of range");
+      if (k > d->row_ptr[i] && d->col_idx[k] <= d->col_idx[k - 1])
+        throw Failure(PS_ERR_BAD_ARG, "problem: columns must be sorted and unique");
+      diag |= d->col_idx[k] == i;
+    }
+    if (!diag) throw Failure(PS_ERR_BAD_ARG, "problem: pattern must contain the diagonal");
+  }
+  if (!(d->period > 0.0)) throw Failure(PS_ERR_BAD_ARG, "problem: excitation period must be positive");
+  // Excitation ctor (proj/src/problem.cpp:36-50)
+  for (int k = 0; k < d->n_terms; ++k) {
+    if (!(d->frequency_hz[k] > 0.0)) throw Failure(PS_ERR_BAD_ARG, "problem: excitation frequency must be positive");
+    const double cycles = d->frequency_hz[k] * d->period;
+    if (std::abs(cycles - std::round(cycles)) > 1e-9 * std::max(1.0, cycles))
+      throw Failure(PS_ERR_BAD_ARG, "problem: excitation frequency is not an integer multiple of 1/period");
+  }
+  if (!d->stiffness) {
+    if (d->nodes_per_elem != 2 && d->nodes_per_elem != 3)
+      throw Failure(PS_ERR_BAD_ARG, "problem: nonlinear problems need 2- or 3-node elements");
+    if (d->n_curves < 1 || d->n_curves > kMaxCurves) throw Failure(PS_ERR_BAD_ARG, "problem: 1..8 curves supported");
+    for (int e = 0; e < d->n_elem; ++e)
+      if (d->elem_curve[e] < 0 || d->elem_curve[e] >= d->n_curves)
+        throw Failure(PS_ERR_BAD_ARG, "problem: element curve index out of range");
+  }
+}
+
+template <class T>
+T* upload(const T* src, size_t n, const char* what) {
+  T* d = nullptr;
+  if (!dalloc(&d, n)) throw Failure(PS_ERR_CUDA, std::string("cuda: out of memory for ") + what);
+  if (n) check(cudaMemcpy(d, src, n * sizeof(T), cudaMemcpyHostToDevice), what);
+  return d;
+}
+
+void build_problem(ps_ctx* ctx, const ps_problem_desc* desc) {
+  DevProblem& P = ctx->P;
+  P.d = desc->dim;
+  P.nnz = desc->nnz;
+  P.linear = desc->stiffness != nullptr;
+  P.h_rp.assign(desc->row_ptr, desc->row_ptr + P.d + 1);
+  P.h_ci.assign(desc->col_idx, desc->col_idx + P.nnz);
+  P.h_M.assign(desc->mass, desc->mass + P.nnz);
+  P.h_diag.resize(P.d);
+  P.max_row_len = 0;
+  for (int i = 0; i < P.d; ++i) {
+    P.max_row_len = std::max(P.max_row_len, P.h_rp[i + 1] - P.h_rp[i]);
+    for (int k = P.h_rp[i]; k < P.h_rp[i + 1]; ++k)
+      if (P.h_ci[k] == i) P.h_diag[i] = k;
+  }
+  P.rp = upload(P.h_rp.data(), P.h_rp.size(), "row_ptr");
+  P.ci = upload(P.h_ci.data(), P.h_ci.size(), "col_idx");
+  P.diag = upload(P.h_diag.data(), P.h_diag.size(), "diag");
+  P.M = upload(P.h_M.data(), P.h_M.size(), "mass");
+  if (P.linear) {
+    P.h_K.assign(desc->stiffness, desc->stiffness + P.nnz);
+    P.K = upload(P.h_K.data(), P.h_K.size(), "stiffness");
+  } else {
+    P.npe = desc->nodes_per_elem;
+    P.ne = desc->n_elem;
+    const int npe = P.npe;
+    const int64_t ne = P.ne;
+    P.en = upload(desc->elem_nodes, ne * npe, "elements");
+    P.eS = upload(desc->elem_stiff, ne * npe * npe, "element stiffness");
+    P.einvA = upload(desc->elem_inv_area, ne, "element areas");
+    P.ecurve = upload(desc->elem_curve, ne, "element curves");
+    P.curves.assign(desc->curves, desc->curves + desc->n_curves);
+    // node -> (element, local index) adjacency in increasing element order,
+    // plus the slot offset of every (a, b) coupling within row a
+    std::vector<int> cnt(P.d + 1, 0);
+    for (int64_t e = 0; e < ne; ++e)
+      for (int a = 0; a < npe; ++a) {
+        const int n = desc->elem_nodes[e * npe + a];
+        if (n >= 0) cnt[n + 1]++;
+      }
+    for (int i = 0; i < P.d; ++i) cnt[i + 1] += cnt[i];
+    std::vector<int2> adj(cnt[P.d]);
+    std::vector<int> rel(static_cast<size_t>(cnt[P.d]) * npe, -1);
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t e = 0; e < ne; ++e)
+      for (int a = 0; a < npe; ++a) {
+        const int n = desc->elem_nodes[e * npe + a];
+        if (n < 0) continue;
+        const int q = fill[n]++;
+        adj[q] = make_int2(static_cast<int>(e), a);
+        for (int b = 0; b < npe; ++b) {
+          const int nb = desc->elem_nodes[e * npe + b];
+          if (nb < 0) continue;
+          const auto first = P.h_ci.begin() + P.h_rp[n], last = P.h_ci.begin() + P.h_rp[n + 1];
+          const auto it = std::lower_bound(first, last, nb);
+          if (it == last || *it != nb) throw Failure(PS_ERR_BAD_ARG, "problem: element coupling missing from pattern");
+          rel[static_cast<size_t>(q) * npe + b] = static_cast<int>(it - first);
+        }
+      }
+    P.adj_ptr = upload(cnt.data(), cnt.size(), "adjacency");
+    P.adj = upload(adj.data(), adj.size(), "adjacency");
+    P.adj_rel = upload(rel.data(), rel.size(), "adjacency slots");
+  }
+  P.nterms = desc->n_terms;
+  P.period = desc->period;
+  P.amp.assign(desc->amplitude, desc->amplitude + P.nterms);
+  P.freq.assign(desc->frequency_hz, desc->frequency_hz + P.nterms);
+  P.phase.assign(desc->phase_rad, desc->phase_rad + P.nterms);
+  P.pat = upload(desc->patterns, static_cast<size_t>(P.nterms) * P.d, "excitation patterns");
+}
+
+void alloc_work(ps_ctx* ctx) {
+  const size_t n = static_cast<size_t>(ctx->P.d) * ctx->max_batch;
+  bool ok = dalloc(&ctx->u, n) && dalloc(&ctx->uprev, n) && dalloc(&ctx->x, n) && dalloc(&ctx->r, n) &&
+            dalloc(&ctx->p, n) && dalloc(&ctx->q, n) && dalloc(&ctx->io_a, n) && dalloc(&ctx->io_b, n);
+  ok = ok && dalloc(&ctx->Dinv, n);
+  if (!ctx->P.linear) ok = ok && dalloc(&ctx->A, static_cast<size_t>(ctx->P.nnz) * ctx->max_batch);
+  ok = ok && dalloc(&ctx->abort_flag, 1) && dalloc(&ctx->out, ctx->max_batch) &&
+       dalloc(&ctx->lockstep, (ctx->max_batch + 31) / 32 + 1);
+  if (!ok) throw Failure(PS_ERR_CUDA, "cuda: out of device memory for the work vectors");
+}
+
+void ensure(double** buf, size_t* len, size_t need) {
+  if (*len >= need) return;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  if (!dalloc(buf, need)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+  *len = need;
+}
+
+Geometry& geometry(ps_ctx* ctx, int count) {
+  auto it = ctx->geo.find(count);
+  if (it != ctx->geo.end()) return it->second;
+  // One warp lane per system (R = 1) and a block count C fixed by (d, max_batch):
+  // every call on this context uses the same per-system reduction tree, so a
+  // system's result is bitwise independent of how the batch is split
+  // (proj/tests/test_engine.cpp:253-271 contract).
+  Geometry g;
+  g.G = (count + 31) / 32;
+  g.L = (count + g.G - 1) / g.G;
+  g.Lp = 32;
+  g.R = 1;
+  const int g_max = (ctx->max_batch + 31) / 32;
+  const int rows_min = kWarps * 4;
+  if (g_max > ctx->capacity) throw Failure(PS_ERR_BAD_ARG, "propagator: batch too large for one cooperative launch");
+  g.C = std::max(1, std::min(ctx->capacity / g_max, (ctx->P.d + rows_min - 1) / rows_min));
+  std::vector<int> ranges;
+  row_ranges(ctx->P.h_rp, g.C, g.R, &ranges);
+  g.warp_row_begin = upload(ranges.data(), ranges.size(), "row ranges");
+  return ctx->geo.emplace(count, g).first->second;
+}
+
+std::pair<double*, double*> shared_step_matrix(ps_ctx* ctx, double dt) {
+  auto it = ctx->step_cache.find(dt);
+  if (it != ctx->step_cache.end()) return it->second;
+  const DevProblem& P = ctx->P;
+  std::vector<double> A(P.nnz), D(P.d);
+  for (int k = 0; k < P.nnz; ++k) A[k] = P.h_M[k] / dt + P.h_K[k];
+  for (int i = 0; i < P.d; ++i) D[i] = 1.0 / A[P.h_diag[i]];
+  auto pr = std::make_pair(upload(A.data(), A.size(), "step matrix"), upload(D.data(), D.size(), "jacobi"));
+  return ctx->step_cache.emplace(dt, pr).first->second;
+}
+
+void excitation_coef(const DevProblem& P, double t, double* out) {
+  // Excitation::operator() (proj/src/problem.cpp:52-63): same double expressions
+  double tau = std::fmod(t, P.period);
+  if (tau < 0.0) tau += P.period;
+  for (int k = 0; k < P.nterms; ++k) {
+    const double arg = 2.0 * kPi * P.freq[k] * tau + P.phase[k];
+    out[k] = P.amp[k] * std::sin(arg);
+  }
+}
+
+const char* failure_what(int code) {
+  switch (code) {
+    case PS_ERR_SINGULAR: return "step system singular";
+    case PS_ERR_NEWTON_MAXITER: return "Newton did not converge";
+    case PS_ERR_NEWTON_DIVERGED: return "Newton iteration diverged";
+    case PS_ERR_PCG_MAXITER: return "PCG did not converge";
+    default: return "step failed";
+  }
+}
+
+struct PropResult {
+  double* state = nullptr;  // interleaved result (stride = count)
+};
+
+// Runs `steps` implicit-Euler steps of size dt for `count` systems whose
+// start states are in ctx->u (interleaved, stride count).  t_next is
+// [steps][count].  newton_mode: run Newton even for linear problems
+// (newton_step semantics) instead of the linear fast path.
+PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::vector<double>& t_next,
+                     bool newton_mode, bool want_trace, ps_batch_status* status) {
+  const DevProblem& P = ctx->P;
+  if (count < 1 || count > ctx->max_batch) throw Failure(PS_ERR_BAD_ARG, "propagator: batch count out of range");
+  if (!(dt > 0.0)) throw Failure(PS_ERR_BAD_ARG, "propagator: step size must be positive");
+  const ps_solver_settings& S = ctx->settings;
+  if (S.newton.max_iter < 1) throw Failure(PS_ERR_BAD_ARG, "propagator: Newton needs at least one iteration");
+  Geometry& geo = geometry(ctx, count);
+  const bool linear_path = P.linear && !newton_mode;
+  if (!linear_path && !ctx->A && !dalloc(&ctx->A, static_cast<size_t>(P.nnz) * ctx->max_batch))
+    throw Failure(PS_ERR_CUDA, "cuda: out of device memory for the step matrices");
+  const int nt = std::max(1, P.nterms);
+  std::vector<double> coef(static_cast<size_t>(steps) * count * nt, 0.0);
+  for (int j = 0; j < steps; ++j)
+    for (int n = 0; n < count; ++n)
+      excitation_coef(P, t_next[static_cast<size_t>(j) * count + n], &coef[(static_cast<size_t>(j) * count + n) * nt]);
+  ensure(&ctx->coef, &ctx->coef_len, coef.size());
+  ensure(&ctx->tnext, &ctx->tnext_len, t_next.size());
+  check(cudaMemcpyAsync(ctx->coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),
+        "coef upload");
+  check(cudaMemcpyAsync(ctx->tnext, t_next.data(), t_next.size() * sizeof(double), cudaMemcpyHostToDevice,
+                        ctx->stream),
+        "t upload");
+  const size_t plen = static_cast<size_t>(2) * geo.G * geo.C * kNDots * 32;
+  ensure(&ctx->partials, &ctx->partials_len, plen);
+  if (!ctx->sync && !dalloc(&ctx->sync, 64)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+  if (geo.G > 64) throw Failure(PS_ERR_BAD_ARG, "propagator: batch too large");
+  if (want_trace) {
+    if (ctx->trace) cudaFree(ctx->trace);
+    if (!dalloc(&ctx->trace, static_cast<size_t>(count) * S.newton.max_iter))
+      throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+    check(cudaMemsetAsync(ctx->trace, 0, static_cast<size_t>(count) * S.newton.max_iter * sizeof(double), ctx->stream),
+          "trace");
+  }
+  check(cudaMemsetAsync(ctx->sync, 0, geo.G * sizeof(unsigned long long), ctx->stream), "sync reset");
+  check(cudaMemsetAsync(ctx->abort_flag, 0, sizeof(int), ctx->stream), "abort reset");
+
+  PropParams K{};
+  K.d = P.d;
+  K.nnz = P.nnz;
+  K.stride = count;
+  K.count = count;
+  K.G = geo.G;
+  K.C = geo.C;
+  K.L = geo.L;
+  K.Lp = geo.Lp;
+  K.R = geo.R;
+  K.warp_row_begin = geo.warp_row_begin;
+  K.rp = P.rp;
+  K.ci = P.ci;
+  K.diag = P.diag;
+  K.M = P.M;
+  K.Klin = P.K;
+  if (linear_path) {
+    const auto sm = shared_step_matrix(ctx, dt);
+    K.Ash = sm.first;
+    K.Dsh = sm.second;
+  }
+  K.adj_ptr = P.adj_ptr;
+  K.adj = P.adj;
+  K.adj_rel = P.adj_rel;
+  K.en = P.en;
+  K.eS = P.eS;
+  K.einvA = P.einvA;
+  K.ecurve = P.ecurve;
+  K.ncurves = static_cast<int>(P.curves.size());
+  for (int k = 0; k < K.ncurves; ++k) K.curves[k] = P.curves[k];
+  K.nterms = P.nterms;
+  K.pat = P.pat;
+  K.coef = ctx->coef;
+  K.t_next = ctx->tnext;
+  K.steps = steps;
+  K.dt = dt;
+  K.u = ctx->u;
+  K.uprev = ctx->uprev;
+  K.ubuf0 = ctx->u;
+  K.ubuf1 = ctx->uprev;
+  K.x = ctx->x;
+  K.r = ctx->r;
+  K.p = ctx->p;
+  K.q = ctx->q;
+  K.Dinv = ctx->Dinv;
+  K.A = ctx->A;
+  K.newton_tol_abs = S.newton.tol_abs;
+  K.newton_tol_rel = S.newton.tol_rel;
+  K.damping = S.newton.damping;
+  K.newton_max = S.newton.max_iter;
+  K.line_search = S.newton.line_search;
+  K.pcg_tol = S.pcg.tol_rel;
+  K.pcg_max = S.pcg.max_iter;
+  K.sync = ctx->sync;
+  K.partials = ctx->partials;
+  K.abort_flag = ctx->abort_flag;
+  K.out = ctx->out;
+  K.trace = want_trace ? ctx->trace : nullptr;
+  K.lockstep = ctx->lockstep;
+
+  const int npe = P.linear ? 0 : P.npe;
+  check(cudaEventRecord(ctx->e0, ctx->stream), "event");
+  std::string err;
+  const int rc = launch_propagate(K, linear_path, npe, ctx->stream, &err);
+  if (rc != PS_OK) throw Failure(rc, err);
+  check(cudaEventRecord(ctx->e1, ctx->stream), "event");
+  std::vector<SysOut> outs(count);
+  std::vector<int64_t> lock(geo.G);
+  int abort_h = 0;
+  check(cudaMemcpyAsync(outs.data(), ctx->out, count * sizeof(SysOut), cudaMemcpyDeviceToHost, ctx->stream), "status");
+  check(cudaMemcpyAsync(lock.data(), ctx->lockstep, geo.G * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream),
+        "status");
+  check(cudaMemcpyAsync(&abort_h, ctx->abort_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "status");
+  check(cudaStreamSynchronize(ctx->stream), "propagation kernel");
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, ctx->e0, ctx->e1);
+  if (abort_h) throw Failure(PS_ERR_WATCHDOG, "cuda: device barrier watchdog fired in the propagation kernel");
+
+  ps_batch_status st{};
+  st.failed_index = -1;
+  const double d = P.d, nnz = P.nnz;
+  double bytes = 0.0;
+  for (int n = 0; n < count; ++n) {
+    const SysOut& o = outs[n];
+    st.newton_iterations += o.newton_total;
+    st.pcg_iterations += o.pcg_total;
+    st.max_newton_iterations = std::max(st.max_newton_iterations, o.max_newton);
+    st.max_pcg_iterations = std::max(st.max_pcg_iterations, o.max_pcg);
+    // canonical bytes: Jacobi-PCG iteration Nb(8 nnz + 80 d) (+ shared
+    // 4 nnz + 4(d+1) per batched iteration); fused refill Nb(8 nnz + 48 d) per Newton
+    // iterate; the linear path reads one shared matrix (8 nnz per batched iteration).
+    if (linear_path) {
+      bytes += static_cast<double>(o.pcg_total) * 80.0 * d;
+    } else {
+      bytes += static_cast<double>(o.pcg_total) * (8.0 * nnz + 80.0 * d);
+      bytes += static_cast<double>(o.newton_total + steps) * (8.0 * nnz + 48.0 * d);
+    }
+    if (o.code != PS_OK && st.code == PS_OK) {
+      st.code = o.code;
+      st.failed_index = n;
+      st.t_next = o.t_fail;
+      st.residual = o.residual;
+    }
+  }
+  for (int g = 0; g < geo.G; ++g) {
+    st.lockstep_pcg_iterations += lock[g];
+    bytes += static_cast<double>(lock[g]) * ((linear_path ? 12.0 : 4.0) * nnz + 4.0 * (d + 1.0));
+  }
+  st.algorithmic_bytes = bytes;
+  st.kernel_ms = ms;
+  if (status) *status = st;
+  if (st.code != PS_OK) {
+    std::ostringstream msg;
+    msg << "propagator: " << failure_what(st.code) << " at t = " << st.t_next << " (residual " << st.residual << ")";
+    throw Failure(st.code, msg.str());
+  }
+  PropResult res;
+  res.state = linear_path ? ((steps & 1) ? ctx->uprev : ctx->u) : ctx->u;
+  return res;
+}
+
+__global__ void copy_column_kernel(const double* src, int src_stride, int src_col, double* dst, int dst_stride,
+                                   int dst_col, int d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d) dst[static_cast<size_t>(i) * dst_stride + dst_col] = src[static_cast<size_t>(i) * src_stride + src_col];
+}
+
+void copy_column(const double* src, int src_stride, int src_col, double* dst, int dst_stride, int dst_col, int d,
+                 cudaStream_t st) {
+  copy_column_kernel<<<(d + 255) / 256, 256, 0, st>>>(src, src_stride, src_col, dst, dst_stride, dst_col, d);
+}
+
+std::vector<double> fine_times(const ps_time_mesh& m, int n_first, int count) {
+  const int s = m.fine_steps;
+  std::vector<double> t(static_cast<size_t>(s) * count);
+  const double dt = fine_dt(m);
+  for (int i = 0; i < count; ++i) {
+    const int n = n_first + i;
+    const double t_left = boundary(m, n - 1);
+    for (int j = 1; j <= s; ++j)
+      t[static_cast<size_t>(j - 1) * count + i] = j == s ? boundary(m, n) : t_left + j * dt;
+  }
+  return t;
+}
+
+void check_range(const ps_time_mesh& m, int n_first, int count) {
+  if (count < 1 || n_first < 1 || n_first + count - 1 > m.subintervals)
+    throw Failure(PS_ERR_BAD_ARG, "propagator: subinterval index out of range");
+}
+
+// host [count][d] -> ctx->u interleaved (stride count)
+void stage_in_host(ps_ctx* ctx, const double* U, int count) {
+  const size_t n = static_cast<size_t>(count) * ctx->P.d;
+  check(cudaMemcpyAsync(ctx->io_a, U, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  launch_to_interleaved(ctx->io_a, ctx->u, count, ctx->P.d, count, ctx->stream);
+}
+void stage_in_dev(ps_ctx* ctx, const double* dU, int count) {
+  launch_to_interleaved(dU, ctx->u, count, ctx->P.d, count, ctx->stream);
+}
+void stage_out_host(ps_ctx* ctx, const double* il, double* U, int count) {
+  const size_t n = static_cast<size_t>(count) * ctx->P.d;
+  launch_from_interleaved(il, ctx->io_b, count, ctx->P.d, count, ctx->stream);
+  check(cudaMemcpyAsync(U, ctx->io_b, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  check(cudaStreamSynchronize(ctx->stream), "D2H");
+}
+
+int create_ctx(const ps_problem_desc* desc, const ps_time_mesh* mesh, const ps_solver_settings* settings, void* stream,
+               ps_ctx** out) {
+  *out = nullptr;
+  auto ctx = std::make_unique<ps_ctx>();
+  const int rc = guard(ctx.get(), [&] {
+    require_device();
+    validate_desc(desc);
+    if (!mesh) throw Failure(PS_ERR_BAD_ARG, "mesh: null");
+    if (mesh->subintervals < 2) throw Failure(PS_ERR_BAD_ARG, "mesh: need at least 2 subintervals");
+    if (mesh->fine_steps < 1) throw Failure(PS_ERR_BAD_ARG, "mesh: need at least 1 fine step per subinterval");
+    if (!(mesh->period > 0.0)) throw Failure(PS_ERR_BAD_ARG, "mesh: period must be positive");
+    if (desc->period != mesh->period)
+      throw Failure(PS_ERR_BAD_ARG, "propagator: mesh period does not match the problem");
+    ctx->mesh = *mesh;
+    if (settings) {
+      ctx->settings = *settings;
+    } else {
+      ps_default_settings(&ctx->settings);
+    }
+    ctx->max_batch = ctx->settings.max_batch > 0 ? ctx->settings.max_batch : mesh->subintervals;
+    if (stream) {
+      ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+      ctx->own_stream = true;
+    }
+    check(cudaEventCreate(&ctx->e0), "event");
+    check(cudaEventCreate(&ctx->e1), "event");
+    build_problem(ctx.get(), desc);
+    int cap = 0;
+    if (max_coresident_blocks(ctx->P.linear, ctx->P.linear ? 0 : ctx->P.npe, &cap) != PS_OK || cap < 1)
+      throw Failure(PS_ERR_CUDA, "cuda: cannot size the cooperative propagation kernel");
+    ctx->capacity = cap;
+    alloc_work(ctx.get());
+  });
+  if (rc != PS_OK) {
+    g_global_error = ctx->err;
+    ps_destroy(ctx.release());
+    return rc;
+  }
+  *out = ctx.release();
+  return PS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ps_default_settings(ps_solver_settings* out) {
+  if (!out) return PS_ERR_BAD_ARG;
+  std::memset(out, 0, sizeof(*out));
+  out->newton.tol_abs = 1e-9;
+  out->newton.tol_rel = 1e-8;
+  out->newton.max_iter = 30;
+  out->newton.damping = 1.0;
+  out->newton.line_search = 0;
+  out->pcg.tol_rel = 1e-12;
+  out->pcg.max_iter = 20000;
+  out->cocg.tol_rel = 1e-12;
+  out->cocg.max_iter = 20000;
+  out->max_batch = 0;
+  return PS_OK;
+}
+
+const char* ps_global_error(void) { return g_global_error.c_str(); }
+
+int ps_device_info(char* name, int name_len, int* sm_count, int* cc_major, int* cc_minor) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    g_global_error = "cuda: no CUDA device available";
+    return PS_ERR_CUDA;
+  }
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, 0) != cudaSuccess) return PS_ERR_CUDA;
+  if (name && name_len > 0) {
+    std::strncpy(name, prop.name, name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  return PS_OK;
+}
+
+int ps_create(const ps_problem_desc* problem, const ps_time_mesh* mesh, const ps_solver_settings* settings,
+              void* stream, ps_ctx** out) {
+  if (!out) return PS_ERR_BAD_ARG;
+  return create_ctx(problem, mesh, settings, stream, out);
+}
+
+void ps_destroy(ps_ctx* ctx) {
+  if (!ctx) return;
+  DevProblem& P = ctx->P;
+  void* ptrs[] = {P.rp, P.ci, P.diag, P.M, P.K, P.adj_ptr, P.adj, P.adj_rel, P.en, P.eS, P.einvA, P.ecurve,
+                  P.pat, ctx->u, ctx->uprev, ctx->x, ctx->r, ctx->p, ctx->q, ctx->Dinv, ctx->A, ctx->io_a,
+                  ctx->io_b, ctx->sync, ctx->partials, ctx->abort_flag, ctx->out, ctx->trace, ctx->lockstep,
+                  ctx->coef, ctx->tnext};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& kv : ctx->geo) cudaFree(kv.second.warp_row_begin);
+  for (auto& kv : ctx->step_cache) {
+    cudaFree(kv.second.first);
+    cudaFree(kv.second.second);
+  }
+  if (ctx->spec) spectral_free(ctx->spec);
+  if (ctx->e0) cudaEventDestroy(ctx->e0);
+  if (ctx->e1) cudaEventDestroy(ctx->e1);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* ps_last_error(const ps_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_error.c_str(); }
+int ps_dim(const ps_ctx* ctx) { return ctx ? ctx->P.d : -1; }
+int ps_is_linear(const ps_ctx* ctx) { return ctx && ctx->P.linear ? 1 : 0; }
+
+// frozen_coarse_linearization (proj/src/engine.cpp:66-74)
+int ps_create_frozen(ps_ctx* ctx, const double* u_ref, ps_ctx** out) {
+  if (!ctx || !out) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    const DevProblem& P = ctx->P;
+    std::vector<double> K(P.nnz);
+    if (P.linear) {
+      K = P.h_K;
+    } else {
+      double* dref = nullptr;
+      double* dK = nullptr;
+      if (!dalloc(&dref, P.d) || !dalloc(&dK, P.nnz)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+      if (u_ref)
+        check(cudaMemcpy(dref, u_ref, P.d * sizeof(double), cudaMemcpyHostToDevice), "u_ref");
+      else
+        check(cudaMemset(dref, 0, P.d * sizeof(double)), "u_ref");
+      launch_frozen_K(P, dref, dK, ctx->stream);
+      check(cudaStreamSynchronize(ctx->stream), "frozen K");
+      check(cudaMemcpy(K.data(), dK, P.nnz * sizeof(double), cudaMemcpyDeviceToHost), "frozen K");
+      cudaFree(dref);
+      cudaFree(dK);
+    }
+    ps_problem_desc desc{};
+    desc.dim = P.d;
+    desc.nnz = P.nnz;
+    desc.row_ptr = P.h_rp.data();
+    desc.col_idx = P.h_ci.data();
+    desc.mass = P.h_M.data();
+    desc.stiffness = K.data();
+    desc.period = P.period;
+    desc.n_terms = P.nterms;
+    std::vector<double> pat(static_cast<size_t>(P.nterms) * P.d);
+    if (!pat.empty())
+      check(cudaMemcpy(pat.data(), P.pat, pat.size() * sizeof(double), cudaMemcpyDeviceToHost), "patterns");
+    desc.patterns = pat.data();
+    desc.amplitude = P.amp.data();
+    desc.frequency_hz = P.freq.data();
+    desc.phase_rad = P.phase.data();
+    ps_solver_settings s = ctx->settings;
+    const int rc = create_ctx(&desc, &ctx->mesh, &s, ctx->own_stream ? nullptr : ctx->stream, out);
+    if (rc != PS_OK) throw Failure(rc, g_global_error);
+  });
+}
+
+int ps_newton_step(ps_ctx* ctx, int32_t count, const double* U_prev, const double* t_next, double dt, double* U_out,
+                   int32_t* iterations, double* residual_norms, ps_batch_status* status) {
+  if (!ctx) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    if (count < 1 || count > ctx->max_batch) throw Failure(PS_ERR_BAD_ARG, "propagator: batch count out of range");
+    stage_in_host(ctx, U_prev, count);
+    std::vector<double> t(t_next, t_next + count);
+    ps_batch_status st{};
+    PropResult res;
+    try {
+      res = propagate(ctx, count, 1, dt, t, true, residual_norms != nullptr, &st);
+    } catch (...) {
+      if (status) *status = st;
+      throw;
+    }
+    if (status) *status = st;
+    stage_out_host(ctx, res.state, U_out, count);
+    if (iterations || residual_norms) {
+      std::vector<SysOut> outs(count);
+      check(cudaMemcpy(outs.data(), ctx->out, count * sizeof(SysOut), cudaMemcpyDeviceToHost), "status");
+      if (iterations)
+        for (int n = 0; n < count; ++n) iterations[n] = outs[n].newton_last;
+      if (residual_norms)
+        check(cudaMemcpy(residual_norms, ctx->trace,
+                         static_cast<size_t>(count) * ctx->settings.newton.max_iter * sizeof(double),
+                         cudaMemcpyDeviceToHost),
+              "trace");
+    }
+  });
+}
+
+static int propagate_api(ps_ctx* ctx, int32_t n_first, int32_t count, const double* U_start, double* U_end,
+                         ps_batch_status* status, bool fine, bool dev) {
+  if (!ctx) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    check_range(ctx->mesh, n_first, count);
+    if (count > ctx->max_batch) throw Failure(PS_ERR_BAD_ARG, "propagator: batch count out of range");
+    if (dev)
+      stage_in_dev(ctx, U_start, count);
+    else
+      stage_in_host(ctx, U_start, count);
+    std::vector<double> t;
+    int steps;
+    double dt;
+    if (fine) {
+      t = fine_times(ctx->mesh, n_first, count);
+      steps = ctx->mesh.fine_steps;
+      dt = fine_dt(ctx->mesh);
+    } else {
+      t.resize(count);
+      for (int i = 0; i < count; ++i) t[i] = boundary(ctx->mesh, n_first + i);
+      steps = 1;
+      dt = coarse_dt(ctx->mesh);
+    }
+    ps_batch_status st{};
+    PropResult res;
+    try {
+      res = propagate(ctx, count, steps, dt, t, false, false, &st);
+    } catch (...) {
+      if (status) *status = st;
+      throw;
+    }
+    if (status) *status = st;
+    if (dev) {
+      launch_from_interleaved(res.state, U_end, count, ctx->P.d, count, ctx->stream);
+      check(cudaStreamSynchronize(ctx->stream), "D2D");
+    } else {
+      stage_out_host(ctx, res.state, U_end, count);
+    }
+  });
+}
+
+int ps_fine_propagate_batch(ps_ctx* ctx, int32_t n_first, int32_t count, const double* U_start, double* U_end,
+                            ps_batch_status* status) {
+  return propagate_api(ctx, n_first, count, U_start, U_end, status, true, false);
+}
+int ps_fine_propagate_batch_dev(ps_ctx* ctx, int32_t n_first, int32_t count, const double* dU_start, double* dU_end,
+                                ps_batch_status* status) {
+  return propagate_api(ctx, n_first, count, dU_start, dU_end, status, true, true);
+}
+int ps_coarse_propagate_batch(ps_ctx* ctx, int32_t n_first, int32_t count, const double* U_start, double* U_end,
+                              ps_batch_status* status) {
+  return propagate_api(ctx, n_first, count, U_start, U_end, status, false, false);
+}
+int ps_coarse_propagate_batch_dev(ps_ctx* ctx, int32_t n_first, int32_t count, const double* dU_start,
+                                  double* dU_end, ps_batch_status* status) {
+  return propagate_api(ctx, n_first, count, dU_start, dU_end, status, false, true);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Initial iterate U[0] = 0, U[n] = G_n(U[n-1]) on an interleaved [d][N] buffer.
+void coarse_sweep_il(ps_ctx* ctx, double* U_il, ps_batch_status* total) {
+  const int N = ctx->mesh.subintervals, d = ctx->P.d;
+  check(cudaMemsetAsync(U_il, 0, static_cast<size_t>(d) * N * sizeof(double), ctx->stream), "zero");
+  for (int n = 1; n < N; ++n) {
+    copy_column(U_il, N, n - 1, ctx->u, 1, 0, d, ctx->stream);
+    std::vector<double> t(1, boundary(ctx->mesh, n));
+    ps_batch_status st{};
+    PropResult res = propagate(ctx, 1, 1, coarse_dt(ctx->mesh), t, false, false, &st);
+    copy_column(res.state, 1, 0, U_il, N, n, d, ctx->stream);
+    if (total) {
+      total->pcg_iterations += st.pcg_iterations;
+      total->kernel_ms += st.kernel_ms;
+      total->algorithmic_bytes += st.algorithmic_bytes;
+    }
+  }
+}
+
+void ensure_spectral(ps_ctx* lin, int use_conj, const int32_t* mask, int shift_kind) {
+  if (lin->spec) {
+    spectral_free(lin->spec);
+    lin->spec = nullptr;
+  }
+  std::string err;
+  const int rc = spectral_setup(&lin->spec, lin->P, lin->mesh.subintervals, lin->mesh.period, use_conj, mask,
+                                shift_kind, &err);
+  if (rc != PS_OK) throw Failure(rc, err);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ps_coarse_sweep(ps_ctx* ctx, double* U, ps_batch_status* status) {
+  if (!ctx || !U) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    const int N = ctx->mesh.subintervals, d = ctx->P.d;
+    double* U_il = nullptr;
+    if (!dalloc(&U_il, static_cast<size_t>(N) * d)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+    ps_batch_status st{};
+    try {
+      coarse_sweep_il(ctx, U_il, &st);
+    } catch (...) {
+      cudaFree(U_il);
+      throw;
+    }
+    launch_from_interleaved(U_il, ctx->io_b, N, d, N, ctx->stream);
+    check(cudaMemcpyAsync(U, ctx->io_b, static_cast<size_t>(N) * d * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream),
+          "D2H");
+    check(cudaStreamSynchronize(ctx->stream), "sweep");
+    cudaFree(U_il);
+    if (status) *status = st;
+  });
+}
+
+int ps_assemble_operators(ps_ctx* ctx, int32_t count, const double* U, double* K_values, double* J_values) {
+  if (!ctx) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    const DevProblem& P = ctx->P;
+    if (count < 1 || count > ctx->max_batch) throw Failure(PS_ERR_BAD_ARG, "problem: batch count out of range");
+    const size_t tot = static_cast<size_t>(count) * P.nnz;
+    if (P.linear) {
+      for (int n = 0; n < count; ++n) {
+        if (K_values) std::copy(P.h_K.begin(), P.h_K.end(), K_values + static_cast<size_t>(n) * P.nnz);
+        if (J_values) std::copy(P.h_K.begin(), P.h_K.end(), J_values + static_cast<size_t>(n) * P.nnz);
+      }
+      return;
+    }
+    stage_in_host(ctx, U, count);
+    double *dK = nullptr, *dJ = nullptr;
+    if (!dalloc(&dK, tot) || !dalloc(&dJ, tot)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+    launch_assemble_ops(P, count, ctx->u, dK, dJ, ctx->stream);
+    check(cudaStreamSynchronize(ctx->stream), "assemble");
+    if (K_values) check(cudaMemcpy(K_values, dK, tot * sizeof(double), cudaMemcpyDeviceToHost), "K");
+    if (J_values) check(cudaMemcpy(J_values, dJ, tot * sizeof(double), cudaMemcpyDeviceToHost), "J");
+    cudaFree(dK);
+    cudaFree(dJ);
+  });
+}
+
+int ps_eval_excitation(ps_ctx* ctx, int32_t count, const double* t, double* out) {
+  if (!ctx) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    const DevProblem& P = ctx->P;
+    if (count < 1 || count > ctx->max_batch) throw Failure(PS_ERR_BAD_ARG, "problem: batch count out of range");
+    const int nt = std::max(1, P.nterms);
+    std::vector<double> coef(static_cast<size_t>(count) * nt, 0.0);
+    for (int n = 0; n < count; ++n) excitation_coef(P, t[n], &coef[static_cast<size_t>(n) * nt]);
+    ensure(&ctx->coef, &ctx->coef_len, coef.size());
+    check(cudaMemcpyAsync(ctx->coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),
+          "coef");
+    launch_excitation(P, count, ctx->coef, ctx->u, ctx->stream);
+    stage_out_host(ctx, ctx->u, out, count);
+  });
+}
+
+int ps_mh_setup(ps_ctx* ctx, int32_t use_conjugate_symmetry, const int32_t* bin_mask, int32_t shift_kind) {
+  if (!ctx) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] { ensure_spectral(ctx, use_conjugate_symmetry, bin_mask, shift_kind); });
+}
+
+int ps_assemble_rhs(ps_ctx* ctx, const double* F, const double* G, double* rhs) {
+  if (!ctx) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    if (!ctx->P.linear)
+      throw Failure(PS_ERR_NOT_LINEAR,
+                    "spectral: cyclic system requires a linear problem (freeze the coarse operator first)");
+    if (!ctx->spec) ensure_spectral(ctx, 1, nullptr, 0);
+    const int N = ctx->mesh.subintervals, d = ctx->P.d;
+    const size_t n = static_cast<size_t>(N) * d;
+    check(cudaMemcpyAsync(ctx->io_a, F, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "F");
+    launch_to_interleaved(ctx->io_a, ctx->u, N, d, N, ctx->stream);
+    check(cudaMemcpyAsync(ctx->io_b, G, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "G");
+    launch_to_interleaved(ctx->io_b, ctx->uprev, N, d, N, ctx->stream);
+    if (spectral_assemble_rhs(ctx->spec, ctx->P, ctx->u, ctx->uprev, ctx->x, ctx->stream) != PS_OK)
+      throw Failure(PS_ERR_CUDA, "cuda: assemble_rhs failed");
+    stage_out_host(ctx, ctx->x, rhs, N);
+  });
+}
+
+int ps_mh_solve(ps_ctx* ctx, const double* rhs, double* U, ps_batch_status* status) {
+  if (!ctx) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    if (!ctx->P.linear)
+      throw Failure(PS_ERR_NOT_LINEAR,
+                    "spectral: cyclic system requires a linear problem (freeze the coarse operator first)");
+    if (!ctx->spec) ensure_spectral(ctx, 1, nullptr, 0);
+    const int N = ctx->mesh.subintervals, d = ctx->P.d;
+    const size_t n = static_cast<size_t>(N) * d;
+    check(cudaMemcpyAsync(ctx->io_a, rhs, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "rhs");
+    launch_to_interleaved(ctx->io_a, ctx->x, N, d, N, ctx->stream);
+    std::string err;
+    const int rc = spectral_solve(ctx->spec, ctx->P, ctx->settings.cocg, ctx->x, ctx->u, nullptr, nullptr, status,
+                                  ctx->stream, &err);
+    if (rc != PS_OK) throw Failure(rc, err);
+    stage_out_host(ctx, ctx->u, U, N);
+  });
+}
+
+int ps_pppc_correct(ps_ctx* ctx, const double* F, const double* G, double* U_inout, double* jump,
+                    ps_batch_status* status) {
+  if (!ctx) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    if (!ctx->P.linear)
+      throw Failure(PS_ERR_NOT_LINEAR,
+                    "spectral: cyclic system requires a linear problem (freeze the coarse operator first)");
+    if (!ctx->spec) ensure_spectral(ctx, 1, nullptr, 0);
+    const int N = ctx->mesh.subintervals, d = ctx->P.d;
+    const size_t n = static_cast<size_t>(N) * d;
+    check(cudaMemcpyAsync(ctx->io_a, F, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "F");
+    launch_to_interleaved(ctx->io_a, ctx->u, N, d, N, ctx->stream);
+    check(cudaMemcpyAsync(ctx->io_b, G, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "G");
+    launch_to_interleaved(ctx->io_b, ctx->uprev, N, d, N, ctx->stream);
+    check(cudaMemcpyAsync(ctx->io_a, U_inout, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "U");
+    launch_to_interleaved(ctx->io_a, ctx->q, N, d, N, ctx->stream);
+    if (spectral_assemble_rhs(ctx->spec, ctx->P, ctx->u, ctx->uprev, nullptr, ctx->stream) != PS_OK)
+      throw Failure(PS_ERR_CUDA, "cuda: assemble_rhs failed");
+    std::string err;
+    const int rc =
+        spectral_solve(ctx->spec, ctx->P, ctx->settings.cocg, nullptr, ctx->q, ctx->q, jump, status, ctx->stream, &err);
+    if (rc != PS_OK) throw Failure(rc, err);
+    stage_out_host(ctx, ctx->q, U_inout, N);
+  });
+}
+
+int ps_forward_dft(int32_t n, int32_t d, const double* U, double* spectrum) {
+  return guard(nullptr, [&] {
+    require_device();
+    std::string err;
+    const int rc = dft_forward_standalone(n, d, U, spectrum, &err);
+    if (rc != PS_OK) throw Failure(rc, err);
+  });
+}
+
+int ps_inverse_dft(int32_t n, int32_t d, const double* spectrum, double* U) {
+  return guard(nullptr, [&] {
+    require_device();
+    std::string err;
+    const int rc = dft_inverse_standalone(n, d, spectrum, U, &err);
+    if (rc != PS_OK) throw Failure(rc, err);
+  });
+}
+
+int ps_jump_norm(int32_t count, int32_t d, const double* cur, const double* prev, double* out) {
+  return guard(nullptr, [&] {
+    require_device();
+    if (count < 1 || d < 1) throw Failure(PS_ERR_BAD_ARG, "engine: jump_norm needs two state lists of equal length");
+    const size_t n = static_cast<size_t>(count) * d;
+    double *a = nullptr, *b = nullptr, *ai = nullptr, *bi = nullptr;
+    if (!dalloc(&a, n) || !dalloc(&b, n) || !dalloc(&ai, n) || !dalloc(&bi, n))
+      throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+    check(cudaMemcpy(a, cur, n * sizeof(double), cudaMemcpyHostToDevice), "cur");
+    check(cudaMemcpy(b, prev, n * sizeof(double), cudaMemcpyHostToDevice), "prev");
+    launch_to_interleaved(a, ai, count, d, count, nullptr);
+    launch_to_interleaved(b, bi, count, d, count, nullptr);
+    const int rc = jump_norm_device(count, d, ai, bi, count, out, nullptr);
+    cudaFree(a);
+    cudaFree(b);
+    cudaFree(ai);
+    cudaFree(bi);
+    if (rc != PS_OK) throw Failure(rc, "cuda: jump_norm failed");
+  });
+}
+
+int ps_eval_reluctivity(const ps_curve* curve, int32_t n, const double* b2, double* nu, double* nu_prime) {
+  return guard(nullptr, [&] {
+    require_device();
+    double *db = nullptr, *dn = nullptr, *dp = nullptr;
+    if (!dalloc(&db, n) || !dalloc(&dn, n) || !dalloc(&dp, n)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+    check(cudaMemcpy(db, b2, n * sizeof(double), cudaMemcpyHostToDevice), "b2");
+    launch_eval_curve(*curve, n, db, dn, dp, nullptr);
+    if (nu) check(cudaMemcpy(nu, dn, n * sizeof(double), cudaMemcpyDeviceToHost), "nu");
+    if (nu_prime) check(cudaMemcpy(nu_prime, dp, n * sizeof(double), cudaMemcpyDeviceToHost), "nu'");
+    cudaFree(db);
+    cudaFree(dn);
+    cudaFree(dp);
+  });
+}
+
+// solve_pp_pc with the multiharmonic coarse solver (proj/src/engine.cpp:187-270).
+// All iterates stay in HBM; the host reads back one jump scalar per iteration.
+int ps_pppc_solve(ps_ctx* fine, const ps_engine_settings* settings, const double* frozen_ref, double* U_out,
+                  double* iterates, ps_history* history) {
+  if (!fine || !settings) return PS_ERR_BAD_ARG;
+  ps_ctx* coarse = nullptr;
+  int rc = ps_create_frozen(fine, frozen_ref, &coarse);
+  if (rc != PS_OK) return rc;
+  std::lock_guard<std::mutex> lock(fine->mu);
+  rc = guard(fine, [&] {
+    std::unique_ptr<ps_ctx, void (*)(ps_ctx*)> hold(coarse, ps_destroy);
+    if (!(settings->tol > 0.0)) throw Failure(PS_ERR_BAD_ARG, "engine: tolerance must be positive");
+    if (settings->max_iterations < 1) throw Failure(PS_ERR_BAD_ARG, "engine: need at least one iteration");
+    const int N = fine->mesh.subintervals, d = fine->P.d;
+    if (fine->max_batch < N) throw Failure(PS_ERR_BAD_ARG, "engine: context batch smaller than N");
+    cudaStream_t st = fine->stream;
+    ps_history h;
+    std::memset(&h, 0, sizeof(h));
+    cudaEvent_t t0, t1;
+    check(cudaEventCreate(&t0), "event");
+    check(cudaEventCreate(&t1), "event");
+    check(cudaEventRecord(t0, st), "event");
+    ensure_spectral(coarse, settings->use_conjugate_symmetry, settings->bin_mask, settings->shift_kind);
+    double* U = nullptr;
+    if (!dalloc(&U, static_cast<size_t>(N) * d)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+    std::unique_ptr<double, cudaError_t (*)(void*)> holdU(U, cudaFree);
+    // the coarse context runs on its own stream; order through the host
+    check(cudaStreamSynchronize(st), "sync");
+    ps_batch_status cs{};
+    coarse_sweep_il(coarse, U, &cs);
+    h.coarse_ms += cs.kernel_ms;
+    h.coarse_pcg_iterations += cs.pcg_iterations;
+    check(cudaStreamSynchronize(coarse->stream), "sweep");
+    const size_t nd = static_cast<size_t>(N) * d;
+    for (int k = 0; k < settings->max_iterations; ++k) {
+      // fine batch: F_n(U_{n-1}), all N subintervals in one launch
+      check(cudaMemcpyAsync(fine->u, U, nd * sizeof(double), cudaMemcpyDeviceToDevice, st), "U->fine");
+      ps_batch_status fs{};
+      PropResult fr = propagate(fine, N, fine->mesh.fine_steps, fine_dt(fine->mesh), fine_times(fine->mesh, 1, N),
+                                false, false, &fs);
+      h.fine_ms += fs.kernel_ms;
+      h.fine_pcg_iterations += fs.pcg_iterations;
+      h.newton_iterations += fs.newton_iterations;
+      h.fine_bytes += fs.algorithmic_bytes;
+      // coarse batch: G_n(U_{n-1}) with the frozen linear operator
+      check(cudaMemcpyAsync(coarse->u, U, nd * sizeof(double), cudaMemcpyDeviceToDevice, coarse->stream), "U->coarse");
+      std::vector<double> tc(N);
+      for (int n = 0; n < N; ++n) tc[n] = boundary(fine->mesh, n + 1);
+      ps_batch_status gs{};
+      PropResult gr = propagate(coarse, N, 1, coarse_dt(fine->mesh), tc, false, false, &gs);
+      h.coarse_ms += gs.kernel_ms;
+      h.coarse_pcg_iterations += gs.pcg_iterations;
+      // correction: rhs = Q (F - G) + f, multiharmonic solve, jump (in place on U)
+      if (spectral_assemble_rhs(coarse->spec, coarse->P, fr.state, gr.state, nullptr, coarse->stream) != PS_OK)
+        throw Failure(PS_ERR_CUDA, "cuda: assemble_rhs failed");
+      double jump = 0.0;
+      ps_batch_status ss{};
+      std::string err;
+      const int src = spectral_solve(coarse->spec, coarse->P, coarse->settings.cocg, nullptr, U, U, &jump, &ss,
+                                     coarse->stream, &err);
+      if (src != PS_OK) throw Failure(src, err);
+      h.spectral_ms += ss.kernel_ms;
+      h.cocg_iterations += ss.pcg_iterations;
+      if (k < PS_MAX_HISTORY) h.jumps[k] = jump;
+      h.iterations = k + 1;
+      if (iterates) {
+        launch_from_interleaved(U, fine->io_b, N, d, N, coarse->stream);
+        check(cudaMemcpyAsync(iterates + static_cast<size_t>(k) * nd, fine->io_b, nd * sizeof(double),
+                              cudaMemcpyDeviceToHost, coarse->stream),
+              "iterate");
+        check(cudaStreamSynchronize(coarse->stream), "iterate");
+      }
+      if (jump <= settings->tol) {
+        h.converged = 1;
+        break;
+      }
+    }
+    check(cudaStreamSynchronize(coarse->stream), "sync");
+    check(cudaEventRecord(t1, st), "event");
+    launch_from_interleaved(U, fine->io_b, N, d, N, st);
+    check(cudaMemcpyAsync(U_out, fine->io_b, nd * sizeof(double), cudaMemcpyDeviceToHost, st), "U_out");
+    check(cudaStreamSynchronize(st), "U_out");
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    h.total_ms = ms;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (history) *history = h;
+  });
+  return rc;
+}
+
+// fine_periodicity_defect (proj/src/engine.cpp:272-290)
+int ps_fine_periodicity_defect(ps_ctx* ctx, const double* U, double* defect) {
+  if (!ctx || !U || !defect) return PS_ERR_BAD_ARG;
+  const int N = ctx->mesh.subintervals, d = ctx->P.d;
+  std::vector<double> F(static_cast<size_t>(N) * d);
+  const int rc = ps_fine_propagate_batch(ctx, 1, N, U, F.data(), nullptr);
+  if (rc != PS_OK) return rc;
+  double scale = 0.0;
+  for (int n = 0; n < N; ++n) {
+    double s = 0.0;
+    for (int i = 0; i < d; ++i) s += U[static_cast<size_t>(n) * d + i] * U[static_cast<size_t>(n) * d + i];
+    scale = std::max(scale, std::sqrt(s));
+  }
+  scale = std::max(1.0, scale);
+  double worst = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double* target = U + static_cast<size_t>((n + 1) % N) * d;
+    double s = 0.0;
+    for (int i = 0; i < d; ++i) {
+      const double df = F[static_cast<size_t>(n) * d + i] - target[i];
+      s += df * df;
+    }
+    worst = std::max(worst, std::sqrt(s));
+  }
+  *defect = worst / scale;
+  return PS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+// Internal declarations shared by the device kernels (kernels.cu), the C ABI
+// (capi.cu) and the host PP-PC driver (driver.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pppc_b200.h"
+
+namespace pppc {
+
+constexpr int kWarps = 16;             // warps per block of the persistent kernels
+constexpr int kThreads = kWarps * 32;  // 512
+constexpr int kMaxCurves = 8;
+constexpr int kMaxTerms = 16;
+constexpr int kNDots = 4;
+constexpr int kRegularRow = 8;         // rows with <= 8 slots use register accumulators
+
+// Per-system outcome written by block 0 of every group.
+struct SysOut {
+  int32_t code;
+  int32_t newton_last;     // Newton iterations of the last step
+  double t_fail;
+  double residual;
+  int64_t newton_total;
+  int64_t pcg_total;
+  int32_t max_newton;
+  int32_t max_pcg;
+};
+
+// Everything the persistent propagation kernel needs (passed by value).
+struct PropParams {
+  // geometry of the launch
+  int d, nnz;
+  int stride;      // interleaved stride = batch count N
+  int count;       // systems in the batch
+  int G, C, L, Lp, R;
+  const int* warp_row_begin;  // [C*kWarps + 1] contiguous row ranges per (block, warp)
+  // pattern
+  const int* rp;
+  const int* ci;
+  const int* diag;
+  const double* M;
+  const double* Klin;     // linear K (Newton on a linear problem)
+  // shared (linear) step matrix and Jacobi diagonal
+  const double* Ash;
+  const double* Dsh;
+  // element data (nonlinear)
+  const int* adj_ptr;
+  const int2* adj;        // (element, local index)
+  const int* adj_rel;     // [n_adj*npe] slot offset within the row, -1 Dirichlet
+  const int* en;
+  const double* eS;
+  const double* einvA;
+  const int* ecurve;
+  ps_curve curves[kMaxCurves];
+  int ncurves;
+  // excitation
+  int nterms;
+  const double* pat;       // [nterms][d]
+  const double* coef;      // [steps][count][nterms]
+  const double* t_next;    // [steps][count]
+  int steps;
+  double dt;
+  // state (interleaved [d][stride]); nonlinear: u (state), uprev; linear: ubuf[2]
+  double* u;
+  double* uprev;
+  double* ubuf0;
+  double* ubuf1;
+  double* x;
+  double* r;
+  double* p;
+  double* q;
+  double* Dinv;   // per-system Jacobi (nonlinear)
+  double* A;      // per-system step-matrix values [nnz][stride] (nonlinear)
+  // settings
+  double newton_tol_abs, newton_tol_rel, damping;
+  int newton_max;
+  int line_search;
+  double pcg_tol;
+  int pcg_max;
+  // sync + outputs
+  unsigned long long* sync;   // [G] monotone arrival counters
+  double* partials;           // [2][G][C][kNDots][32]
+  int* abort_flag;
+  SysOut* out;                // [count]
+  double* trace;              // [count][newton_max] or null
+  int64_t* lockstep;          // [G] lock-step PCG iterations executed
+};
+
+struct DftPlan;
+
+// Device-resident problem + work buffers owned by a context.
+struct DevProblem {
+  int d = 0, nnz = 0;
+  bool linear = true;
+  int npe = 0;
+  int ne = 0;
+  int* rp = nullptr;
+  int* ci = nullptr;
+  int* diag = nullptr;
+  double* M = nullptr;
+  double* K = nullptr;        // linear K (or frozen K-bar)
+  int* adj_ptr = nullptr;
+  int2* adj = nullptr;
+  int* adj_rel = nullptr;
+  int* en = nullptr;
+  double* eS = nullptr;
+  double* einvA = nullptr;
+  int* ecurve = nullptr;
+  std::vector<ps_curve> curves;
+  int nterms = 0;
+  double* pat = nullptr;
+  double period = 0.0;
+  std::vector<double> amp, freq, phase;
+  // host copies needed for setup
+  std::vector<int> h_rp, h_ci, h_diag;
+  std::vector<double> h_M, h_K;
+  int max_row_len = 0;
+};
+
+// launches (kernels.cu)
+int launch_propagate(const PropParams& prm, bool linear, int npe, cudaStream_t st, std::string* err);
+int max_coresident_blocks(bool linear, int npe, int* out);
+void launch_to_interleaved(const double* src, double* dst, int count, int d, int stride,
+                           cudaStream_t st);
+void launch_from_interleaved(const double* src, double* dst, int count, int d, int stride,
+                             cudaStream_t st);
+void launch_assemble_ops(const DevProblem& p, int count, const double* u_il, double* K_out,
+                         double* J_out, cudaStream_t st);
+void launch_excitation(const DevProblem& p, int count, const double* coef, double* out_il,
+                       cudaStream_t st);
+void launch_fill(double* dst, double v, size_t n, cudaStream_t st);
+void launch_axpby_shared(const double* a, double sa, const double* b, double sb, double* out,
+                         size_t n, cudaStream_t st);
+void launch_eval_curve(const ps_curve& c, int n, const double* b2, double* nu, double* nup,
+                       cudaStream_t st);
+void launch_frozen_K(const DevProblem& p, const double* u_ref, double* K_out, cudaStream_t st);
+
+// spectral (spectral.cu)
+struct SpectralState;
+int spectral_setup(SpectralState** out, const DevProblem& p, int N, double period,
+                   int use_conj, const int32_t* mask, int shift_kind, std::string* err);
+void spectral_free(SpectralState* s);
+int spectral_assemble_rhs(SpectralState* s, const DevProblem& p, const double* F_il,
+                          const double* G_il, double* rhs_il, cudaStream_t st);
+int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settings& cocg,
+                   const double* rhs_il, double* U_il, double* U_prev_il, double* jump,
+                   ps_batch_status* status, cudaStream_t st, std::string* err);
+int dft_forward_standalone(int n, int d, const double* U, double* spec, std::string* err);
+int dft_inverse_standalone(int n, int d, const double* spec, double* U, std::string* err);
+int jump_norm_device(int count, int d, const double* cur_il, const double* prev_il, int stride,
+                     double* out, cudaStream_t st);
+
+}  // namespace pppc

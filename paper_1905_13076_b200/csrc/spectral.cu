@@ -1,0 +1,825 @@
+// Multiharmonic coarse solve on B200 (sm_100a), fp64.
+//
+//   rhs_row = Q (F_sub - G_sub) + f(T_sub)           assemble_rhs, proj/src/spectral.cpp:134-150
+//   rhs_hat = unitary DFT across rows (per DOF)      dft_bins,     proj/src/spectral.cpp:32-63
+//   Lambda_p x_p = rhs_hat_p  for every solved bin    MultiharmonicCyclicSolver::solve, :257-279
+//   U = realify(IDFT(mirror(x)))                      :72-84, :270-278
+//   jump = max_n |U_n - U_old_n| / max(1, max_n |U_n|)   jump_norm, proj/src/engine.cpp:54-64
+//
+// The per-bin complex sparse LU of the reference is replaced by a batched
+// Jacobi-preconditioned COCG (complex-symmetric CG, unconjugated bilinear form)
+// running as one persistent kernel over all bins: lane = bin, the block matrix
+// Lambda_p = X + s_p Y is never materialised — X = Q and Y = C (= M/dT) are read
+// once per slot for all bins of a warp and shifted on the fly.
+#include "group_sync.cuh"
+#include "pppc_internal.h"
+
+#include <cmath>
+#include <complex>
+#include <cstring>
+
+namespace pppc {
+
+namespace {
+
+constexpr int kCND = 6;  // complex dots: 3 complex values per reduction at most
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kImagResidualTol = 1e-8;  // proj/src/spectral.cpp:21
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  const double den = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
+}
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+
+struct CocgParams {
+  int d, H;   // DOFs, solved bins (interleave stride)
+  int G, C, L, Lp, R;
+  const int* warp_row_begin;
+  const int* rp;
+  const int* ci;
+  const int* diag;
+  const double* X;  // Q (or K)
+  const double* Y;  // C = M/dT (or M)
+  const double2* shift;  // [H] Lambda_b = X + shift_b * Y
+  const double2* b;      // rhs_hat [d][H]
+  double2* x;
+  double2* r;
+  double2* p;
+  double2* q;
+  double tol;
+  int max_iter;
+  unsigned long long* sync;
+  double* partials;
+  int* abort_flag;
+  int* code;       // [H]
+  int* iters;      // [H]
+  int64_t* lockstep;
+};
+
+struct BinLane {
+  bool alive, act;
+  int code, it;
+  double2 rho, alpha, beta;
+  double stop;
+};
+
+__device__ __forceinline__ double2 lam_diag(const CocgParams& P, int i, double2 s) {
+  const int k = __ldg(P.diag + i);
+  const double xv = __ldg(P.X + k), yv = __ldg(P.Y + k);
+  return make_double2(xv + s.x * yv, s.y * yv);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
+  __shared__ SyncShared<kCND> sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x / P.C, c = blockIdx.x % P.C;
+  const int sub = lane / P.Lp, sl = lane % P.Lp;
+  const int h = g * P.L + sl;
+  const bool valid = (sl < P.L) && (h < P.H);
+  if (threadIdx.x == 0) sh.abort = 0;
+  __syncthreads();
+  SyncCtx X;
+  X.sync = P.sync;
+  X.partials = P.partials;
+  X.abort_flag = P.abort_flag;
+  X.G = P.G;
+  X.C = P.C;
+  X.Lp = P.Lp;
+  const int row_begin = P.warp_row_begin[c * kWarps + warp];
+  const int row_end = P.warp_row_begin[c * kWarps + warp + 1];
+  unsigned long long target = 0;
+  int bar_idx = 0;
+  const size_t H = static_cast<size_t>(P.H);
+  const double2 s_b = valid ? P.shift[h] : make_double2(0.0, 0.0);
+  double acc[kCND] = {0, 0, 0, 0, 0, 0};
+
+  BinLane s;
+  s.alive = valid;
+  s.act = false;
+  s.code = PS_OK;
+  s.it = 0;
+  s.rho = s.alpha = s.beta = make_double2(0.0, 0.0);
+  s.stop = 0.0;
+  long long lockstep = 0;
+
+  // init: x = 0, r = b, z = D r, p = z, rho = r.z, bb = |r|^2
+  if (s.alive)
+    for (int i = row_begin + sub; i < row_end; i += P.R) {
+      const size_t iv = static_cast<size_t>(i) * H + h;
+      const double2 bv = P.b[iv];
+      const double2 z = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
+      const double2 zr = cmul(z, bv);
+      P.x[iv] = make_double2(0.0, 0.0);
+      P.r[iv] = bv;
+      P.p[iv] = zr;
+      const double2 rz = cmul(bv, zr);
+      acc[0] += rz.x;
+      acc[1] += rz.y;
+      acc[2] += bv.x * bv.x + bv.y * bv.y;
+    }
+  if (!group_sync_reduce<kCND, 3>(X, sh, acc, g, c, target, bar_idx)) return;
+  if (s.alive) {
+    s.rho = make_double2(sh.tot[0][sl], sh.tot[1][sl]);
+    const double bb = sh.tot[2][sl];
+    s.stop = (P.tol * P.tol) * bb;
+    s.act = bb != 0.0;
+  }
+
+  while (__syncthreads_or(s.act ? 1 : 0)) {
+    if (s.act)
+      for (int i = row_begin + sub; i < row_end; i += P.R) {
+        const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+        double2 qv = make_double2(0.0, 0.0);
+        for (int k = base; k < end; ++k) {
+          const int j = __ldg(P.ci + k);
+          const double xv = __ldg(P.X + k), yv = __ldg(P.Y + k);
+          const double2 lam = make_double2(xv + s_b.x * yv, s_b.y * yv);
+          qv = cadd(qv, cmul(lam, P.p[static_cast<size_t>(j) * H + h]));
+        }
+        const size_t iv = static_cast<size_t>(i) * H + h;
+        P.q[iv] = qv;
+        const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
+        const double2 pi = P.p[iv], ri = P.r[iv];
+        const double2 zi = cmul(dinv, ri);
+        const double2 pq = cmul(pi, qv), qz = cmul(qv, zi), qdq = cmul(qv, cmul(dinv, qv));
+        acc[0] += pq.x;
+        acc[1] += pq.y;
+        acc[2] += qz.x;
+        acc[3] += qz.y;
+        acc[4] += qdq.x;
+        acc[5] += qdq.y;
+      }
+    if (!group_sync_reduce<kCND, 6>(X, sh, acc, g, c, target, bar_idx)) return;
+    ++lockstep;
+    if (s.act) {
+      const double2 mu = make_double2(sh.tot[0][sl], sh.tot[1][sl]);
+      const double2 qz = make_double2(sh.tot[2][sl], sh.tot[3][sl]);
+      const double2 qdq = make_double2(sh.tot[4][sl], sh.tot[5][sl]);
+      if (!isfinite(mu.x) || !isfinite(mu.y) || (mu.x == 0.0 && mu.y == 0.0)) {
+        s.alive = s.act = false;
+        s.code = PS_ERR_SINGULAR_BLOCK;
+      } else {
+        s.alpha = cdiv(s.rho, mu);
+        // rho_est = rho - 2 alpha qz + alpha^2 qdq
+        const double2 t1 = cmul(cscale(2.0, s.alpha), qz);
+        const double2 t2 = cmul(cmul(s.alpha, s.alpha), qdq);
+        const double2 rho_est = cadd(csub(s.rho, t1), t2);
+        s.beta = cdiv(rho_est, s.rho);
+      }
+    }
+    if (s.act)
+      for (int i = row_begin + sub; i < row_end; i += P.R) {
+        const size_t iv = static_cast<size_t>(i) * H + h;
+        const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
+        const double2 pi = P.p[iv], qi = P.q[iv];
+        double2 ri = P.r[iv];
+        P.x[iv] = cadd(P.x[iv], cmul(s.alpha, pi));
+        ri = csub(ri, cmul(s.alpha, qi));
+        const double2 zi = cmul(dinv, ri);
+        P.r[iv] = ri;
+        P.p[iv] = cadd(zi, cmul(s.beta, pi));
+        const double2 rz = cmul(ri, zi);
+        acc[0] += ri.x * ri.x + ri.y * ri.y;
+        acc[1] += rz.x;
+        acc[2] += rz.y;
+      }
+    if (!group_sync_reduce<kCND, 3>(X, sh, acc, g, c, target, bar_idx)) return;
+    if (s.act) {
+      const double rr = sh.tot[0][sl];
+      s.rho = make_double2(sh.tot[1][sl], sh.tot[2][sl]);
+      s.it += 1;
+      if (rr <= s.stop) {
+        s.act = false;
+      } else if (!isfinite(rr)) {
+        s.alive = s.act = false;
+        s.code = PS_ERR_SINGULAR_BLOCK;
+      } else if (s.it >= P.max_iter) {
+        s.alive = s.act = false;
+        s.code = PS_ERR_COCG_MAXITER;
+      }
+    }
+  }
+  if (c == 0 && warp == 0 && sub == 0 && valid) {
+    P.code[h] = s.code;
+    P.iters[h] = s.it;
+  }
+  if (c == 0 && threadIdx.x == 0) P.lockstep[g] = lockstep;
+}
+
+// rhs[i][row] = sum_k Q_k (F[c_k][sub-1] - G[c_k][sub-1]) + f_i(T_sub)
+__global__ void assemble_rhs_kernel(int d, int N, const int* __restrict__ rp, const int* __restrict__ ci,
+                                    const double* __restrict__ Q, const double* F, const double* Gv,
+                                    const double* __restrict__ pat, const double* __restrict__ coef, int nterms,
+                                    double* rhs) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(d) * N) return;
+  const int row = static_cast<int>(t % N), i = static_cast<int>(t / N);
+  const int sub = row == 0 ? N : row;
+  double acc = 0.0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    const size_t j = static_cast<size_t>(ci[k]) * N + (sub - 1);
+    acc += Q[k] * (F[j] - Gv[j]);
+  }
+  double f = 0.0;
+  for (int k = 0; k < nterms; ++k) f += coef[static_cast<size_t>(row) * nterms + k] * pat[static_cast<size_t>(k) * d + i];
+  rhs[t] = acc + f;
+}
+
+// rhs_hat[i][h] = N^{-1/2} sum_n rhs[i][n] exp(-2 pi i bin_h n / N)
+__global__ void dft_forward_kernel(int d, int N, int H, const int* __restrict__ bins, const double2* __restrict__ tw,
+                                   const double* rhs, double2* out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(d) * H) return;
+  const int hh = static_cast<int>(t % H), i = static_cast<int>(t / H);
+  const int b = bins[hh];
+  const double* row = rhs + static_cast<size_t>(i) * N;
+  double ar = 0.0, ai = 0.0;
+  int idx = 0;
+  for (int n = 0; n < N; ++n) {
+    const double v = row[n];
+    const double2 w = tw[idx];
+    ar += v * w.x;
+    ai += v * w.y;
+    idx += b;
+    if (idx >= N) idx -= N;
+  }
+  const double scale = 1.0 / sqrt(static_cast<double>(N));
+  out[t] = make_double2(scale * ar, scale * ai);
+}
+
+// U_new[i][n] = N^{-1/2} sum over the (mirrored) spectrum, realified; fused with
+// the jump partials (per-block, per-n sums of |U_new - U_old|^2 and |U_new|^2)
+// and the max |re| / max |im| of the realify check.
+__global__ void idft_jump_kernel(int d, int N, int H, const int* __restrict__ bins, const double2* __restrict__ tw,
+                                 int conj, const double2* xhat, double* U, const double* U_old, double* part,
+                                 double* maxre, double* maxim) {
+  extern __shared__ double smem[];  // [2][nwarps][N]
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double scale = 1.0 / sqrt(static_cast<double>(N));
+  double mre = 0.0, mim = 0.0;
+  for (int n = 0; n < N; ++n) {
+    double vr = 0.0, vi = 0.0;
+    if (i < d) {
+      for (int hh = 0; hh < H; ++hh) {
+        const int b = bins[hh];
+        const double2 xv = xhat[static_cast<size_t>(i) * H + hh];
+        const double2 w = tw[(static_cast<int64_t>(b) * n) % N];  // exp(-2 pi i b n/N); inverse uses conj
+        // xv * conj(w)
+        const double cr = xv.x * w.x + xv.y * w.y;
+        const double cim = xv.y * w.x - xv.x * w.y;
+        if (conj && b != 0 && 2 * b != N) {
+          vr += 2.0 * cr;
+        } else {
+          vr += cr;
+          vi += cim;
+        }
+      }
+      vr *= scale;
+      vi *= scale;
+      mre = fmax(mre, fabs(vr));
+      mim = fmax(mim, fabs(vi));
+    }
+    double dd = 0.0, nn = 0.0;
+    if (i < d) {
+      const size_t iv = static_cast<size_t>(i) * N + n;
+      if (U_old) {
+        const double df = vr - U_old[iv];
+        dd = df * df;
+      }
+      nn = vr * vr;
+      U[iv] = vr;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      dd += __shfl_xor_sync(0xffffffffu, dd, off);
+      nn += __shfl_xor_sync(0xffffffffu, nn, off);
+    }
+    if (lane == 0) {
+      smem[(0 * nw + warp) * N + n] = dd;
+      smem[(1 * nw + warp) * N + n] = nn;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, off));
+    mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, off));
+  }
+  __syncthreads();
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    double a = 0.0, b2 = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      a += smem[(0 * nw + w) * N + n];
+      b2 += smem[(1 * nw + w) * N + n];
+    }
+    part[(static_cast<size_t>(blockIdx.x) * 2 + 0) * N + n] = a;
+    part[(static_cast<size_t>(blockIdx.x) * 2 + 1) * N + n] = b2;
+  }
+  if (lane == 0) {
+    maxre[blockIdx.x * nw + warp] = mre;
+    maxim[blockIdx.x * nw + warp] = mim;
+  }
+}
+
+// out[0] = jump, out[1] = max_n |dU_n|, out[2] = max_n |U_n|, out[3] = max|re|, out[4] = max|im|
+__global__ void jump_finalize_kernel(int N, int nblocks, int nmax, const double* part, const double* maxre,
+                                     const double* maxim, double* out) {
+  __shared__ double sd[1024], sn[1024], sr[1024], si[1024];
+  double bd = 0.0, bn = 0.0;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < nblocks; ++k) {
+      a += part[(static_cast<size_t>(k) * 2 + 0) * N + n];
+      b += part[(static_cast<size_t>(k) * 2 + 1) * N + n];
+    }
+    bd = fmax(bd, sqrt(a));
+    bn = fmax(bn, sqrt(b));
+  }
+  double mr = 0.0, mi = 0.0;
+  for (int k = threadIdx.x; k < nmax; k += blockDim.x) {
+    mr = fmax(mr, maxre[k]);
+    mi = fmax(mi, maxim[k]);
+  }
+  sd[threadIdx.x] = bd;
+  sn[threadIdx.x] = bn;
+  sr[threadIdx.x] = mr;
+  si[threadIdx.x] = mi;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double D = 0.0, Nn = 0.0, R = 0.0, I = 0.0;
+    for (int k = 0; k < blockDim.x; ++k) {
+      D = fmax(D, sd[k]);
+      Nn = fmax(Nn, sn[k]);
+      R = fmax(R, sr[k]);
+      I = fmax(I, si[k]);
+    }
+    out[0] = D / fmax(1.0, Nn);
+    out[1] = D;
+    out[2] = Nn;
+    out[3] = R;
+    out[4] = I;
+  }
+}
+
+// generic complex DFT for the standalone forward/inverse entry points:
+// out[b][j] = N^{-1/2} sum_n in[n][j] w^{+-bn}, in/out [N][d] complex
+__global__ void dft_generic_kernel(int N, int d, const double2* __restrict__ tw, int inverse, const double2* in,
+                                   double2* out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(N) * d) return;
+  const int j = static_cast<int>(t % d), b = static_cast<int>(t / d);
+  double ar = 0.0, ai = 0.0;
+  for (int n = 0; n < N; ++n) {
+    double2 w = tw[(static_cast<int64_t>(b) * n) % N];
+    if (inverse) w.y = -w.y;
+    const double2 v = in[static_cast<size_t>(n) * d + j];
+    ar += v.x * w.x - v.y * w.y;
+    ai += v.x * w.y + v.y * w.x;
+  }
+  const double scale = 1.0 / sqrt(static_cast<double>(N));
+  out[t] = make_double2(scale * ar, scale * ai);
+}
+
+__global__ void strided_jump_kernel(int count, int d, int stride, const double* cur, const double* prev,
+                                    double* part) {
+  // one block per system n: part[n][0] = |cur_n - prev_n|^2, part[n][1] = |cur_n|^2
+  __shared__ double sa[256], sb[256];
+  const int n = blockIdx.x;
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const size_t iv = static_cast<size_t>(i) * stride + n;
+    const double c = cur[iv], df = c - prev[iv];
+    a += df * df;
+    b += c * c;
+  }
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sa[threadIdx.x] += sa[threadIdx.x + s];
+      sb[threadIdx.x] += sb[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * n] = sa[0];
+    part[2 * n + 1] = sb[0];
+  }
+}
+
+std::vector<double2> twiddles(int N) {
+  std::vector<double2> tw(N);
+  for (int k = 0; k < N; ++k) {
+    const double ang = 2.0 * kPi * k / N;
+    tw[k] = make_double2(std::cos(ang), -std::sin(ang));
+  }
+  return tw;
+}
+
+template <class T>
+int dalloc(T** p, size_t n) {
+  if (n == 0) n = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)) == cudaSuccess ? PS_OK : PS_ERR_CUDA;
+}
+
+}  // namespace
+
+struct SpectralState {
+  int N = 0, d = 0, nnz = 0, H = 0;
+  double period = 0.0;
+  int conj = 1, shift_kind = 0;
+  std::vector<int> bins;
+  std::vector<int> harmonic;  // signed harmonic index per solved bin
+  int G = 0, C = 0, L = 0, Lp = 0, R = 0;
+  int* warp_row_begin = nullptr;
+  double* X = nullptr;
+  double* Y = nullptr;
+  double* Q = nullptr;  // C + K for the RHS
+  double2* shift = nullptr;
+  double2* tw = nullptr;
+  int* d_bins = nullptr;
+  double* rhs = nullptr;  // [d][N]
+  double2 *bhat = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
+  unsigned long long* sync = nullptr;
+  double* partials = nullptr;
+  int* abort_flag = nullptr;
+  int* code = nullptr;
+  int* iters = nullptr;
+  int64_t* lockstep = nullptr;
+  double* jpart = nullptr;
+  double* maxre = nullptr;
+  double* maxim = nullptr;
+  double* jout = nullptr;
+  double* coef = nullptr;  // [N][nterms] excitation at T_sub per row
+  int idft_blocks = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+// shared with capi.cu
+int row_ranges(const std::vector<int>& h_rp, int C, int R, std::vector<int>* out);
+
+int spectral_setup(SpectralState** out, const DevProblem& p, int N, double period, int use_conj,
+                   const int32_t* mask, int shift_kind, std::string* err) {
+  if (N < 2 || N % 2 != 0) {
+    *err = "spectral: multiharmonic solve requires an even number of blocks >= 2, got " + std::to_string(N);
+    return PS_ERR_ODD_BLOCKS;
+  }
+  if (!p.linear) {
+    *err = "spectral: cyclic system requires a linear problem (freeze the coarse operator first)";
+    return PS_ERR_NOT_LINEAR;
+  }
+  auto* s = new SpectralState();
+  s->N = N;
+  s->d = p.d;
+  s->nnz = p.nnz;
+  s->period = period;
+  s->conj = use_conj ? 1 : 0;
+  s->shift_kind = shift_kind;
+  const int last = use_conj ? N / 2 : N - 1;
+  for (int b = 0; b <= last; ++b) {
+    if (mask && mask[b] == 0) continue;
+    s->bins.push_back(b);
+    s->harmonic.push_back(b <= N / 2 ? b : b - N);
+  }
+  s->H = static_cast<int>(s->bins.size());
+  const double dT = period / N;
+  // host: C = M/dT, Q = C + K  (make_cyclic_system, proj/src/spectral.cpp:118-132)
+  std::vector<double> hC(p.nnz), hQ(p.nnz);
+  for (int k = 0; k < p.nnz; ++k) {
+    hC[k] = p.h_M[k] / dT;
+    hQ[k] = hC[k] + p.h_K[k];
+  }
+  std::vector<double2> hs(std::max(1, s->H));
+  for (int hh = 0; hh < s->H; ++hh) {
+    const int pidx = s->harmonic[hh];
+    if (shift_kind == 0) {
+      const std::complex<double> phase = std::exp(std::complex<double>(0.0, -2.0 * kPi * pidx / N));
+      hs[hh] = make_double2(-phase.real(), -phase.imag());
+    } else {
+      hs[hh] = make_double2(0.0, 2.0 * kPi * pidx / period);
+    }
+  }
+  int rc = PS_OK;
+  rc |= dalloc(&s->X, p.nnz);
+  rc |= dalloc(&s->Y, p.nnz);
+  rc |= dalloc(&s->Q, p.nnz);
+  rc |= dalloc(&s->shift, std::max(1, s->H));
+  rc |= dalloc(&s->tw, N);
+  rc |= dalloc(&s->d_bins, std::max(1, s->H));
+  rc |= dalloc(&s->rhs, static_cast<size_t>(p.d) * N);
+  const size_t cvec = static_cast<size_t>(p.d) * std::max(1, s->H);
+  rc |= dalloc(&s->bhat, cvec);
+  rc |= dalloc(&s->x, cvec);
+  rc |= dalloc(&s->r, cvec);
+  rc |= dalloc(&s->p, cvec);
+  rc |= dalloc(&s->q, cvec);
+  if (rc != PS_OK) {
+    *err = "cuda: out of memory in spectral setup";
+    spectral_free(s);
+    return PS_ERR_CUDA;
+  }
+  if (shift_kind == 0) {
+    cudaMemcpy(s->X, hQ.data(), p.nnz * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpy(s->Y, hC.data(), p.nnz * sizeof(double), cudaMemcpyHostToDevice);
+  } else {
+    cudaMemcpy(s->X, p.h_K.data(), p.nnz * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpy(s->Y, p.h_M.data(), p.nnz * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  cudaMemcpy(s->Q, hQ.data(), p.nnz * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(s->shift, hs.data(), hs.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  const auto tw = twiddles(N);
+  cudaMemcpy(s->tw, tw.data(), N * sizeof(double2), cudaMemcpyHostToDevice);
+  if (s->H > 0) cudaMemcpy(s->d_bins, s->bins.data(), s->H * sizeof(int), cudaMemcpyHostToDevice);
+
+  // COCG launch geometry: groups of <= 32 bins, C co-resident blocks per group
+  if (s->H > 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cocg_kernel, kThreads, 0);
+    const int capacity = std::max(1, sms * per_sm);
+    s->G = (s->H + 31) / 32;
+    s->L = (s->H + s->G - 1) / s->G;
+    s->Lp = 1;
+    while (s->Lp < s->L) s->Lp <<= 1;
+    s->R = 32 / s->Lp;
+    const int rows_min = kWarps * s->R * 4;
+    s->C = std::max(1, std::min(capacity / s->G, (p.d + rows_min - 1) / rows_min));
+    if (s->G > capacity) {
+      *err = "spectral: too many harmonic bins for one cooperative launch";
+      spectral_free(s);
+      return PS_ERR_BAD_ARG;
+    }
+    std::vector<int> ranges;
+    row_ranges(p.h_rp, s->C, s->R, &ranges);
+    rc |= dalloc(&s->warp_row_begin, ranges.size());
+    cudaMemcpy(s->warp_row_begin, ranges.data(), ranges.size() * sizeof(int), cudaMemcpyHostToDevice);
+    rc |= dalloc(&s->sync, s->G);
+    rc |= dalloc(&s->partials, static_cast<size_t>(2) * s->G * s->C * kCND * 32);
+    rc |= dalloc(&s->abort_flag, 1);
+    rc |= dalloc(&s->code, s->H);
+    rc |= dalloc(&s->iters, s->H);
+    rc |= dalloc(&s->lockstep, s->G);
+  }
+  s->idft_blocks = (p.d + 127) / 128;
+  rc |= dalloc(&s->jpart, static_cast<size_t>(s->idft_blocks) * 2 * N);
+  rc |= dalloc(&s->maxre, static_cast<size_t>(s->idft_blocks) * 4);
+  rc |= dalloc(&s->maxim, static_cast<size_t>(s->idft_blocks) * 4);
+  rc |= dalloc(&s->jout, 8);
+  rc |= dalloc(&s->coef, static_cast<size_t>(N) * std::max(1, p.nterms));
+  // excitation coefficients at T_sub for every row (assemble_rhs)
+  std::vector<double> coef(static_cast<size_t>(N) * std::max(1, p.nterms), 0.0);
+  for (int row = 0; row < N; ++row) {
+    const int sub = row == 0 ? N : row;
+    const double t = sub == N ? period : static_cast<double>(sub) * period / N;  // TimeMesh::boundary
+    double tau = std::fmod(t, p.period);
+    if (tau < 0.0) tau += p.period;
+    for (int k = 0; k < p.nterms; ++k) {
+      const double arg = 2.0 * kPi * p.freq[k] * tau + p.phase[k];
+      coef[static_cast<size_t>(row) * p.nterms + k] = p.amp[k] * std::sin(arg);
+    }
+  }
+  cudaMemcpy(s->coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaEventCreate(&s->e0);
+  cudaEventCreate(&s->e1);
+  if (rc != PS_OK || cudaGetLastError() != cudaSuccess) {
+    *err = "cuda: spectral setup failed";
+    spectral_free(s);
+    return PS_ERR_CUDA;
+  }
+  *out = s;
+  return PS_OK;
+}
+
+void spectral_free(SpectralState* s) {
+  if (!s) return;
+  void* ptrs[] = {s->warp_row_begin, s->X, s->Y, s->Q, s->shift, s->tw, s->d_bins, s->rhs, s->bhat,
+                  s->x, s->r, s->p, s->q, s->sync, s->partials, s->abort_flag, s->code, s->iters,
+                  s->lockstep, s->jpart, s->maxre, s->maxim, s->jout, s->coef};
+  for (void* ptr : ptrs)
+    if (ptr) cudaFree(ptr);
+  if (s->e0) cudaEventDestroy(s->e0);
+  if (s->e1) cudaEventDestroy(s->e1);
+  delete s;
+}
+
+int spectral_assemble_rhs(SpectralState* s, const DevProblem& p, const double* F_il, const double* G_il,
+                          double* rhs_il, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(s->d) * s->N;
+  assemble_rhs_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+      s->d, s->N, p.rp, p.ci, s->Q, F_il, G_il, p.pat, s->coef, p.nterms, rhs_il ? rhs_il : s->rhs);
+  return cudaGetLastError() == cudaSuccess ? PS_OK : PS_ERR_CUDA;
+}
+
+int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settings& cocg, const double* rhs_il,
+                   double* U_il, double* U_prev_il, double* jump, ps_batch_status* status, cudaStream_t st,
+                   std::string* err) {
+  const int N = s->N, d = s->d, H = s->H;
+  cudaEventRecord(s->e0, st);
+  const double* rhs = rhs_il ? rhs_il : s->rhs;
+  int64_t lock_total = 0, its_total = 0;
+  int max_its = 0;
+  if (H > 0) {
+    const int64_t tot = static_cast<int64_t>(d) * H;
+    dft_forward_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(d, N, H, s->d_bins, s->tw, rhs,
+                                                                                 s->bhat);
+    cudaMemsetAsync(s->sync, 0, s->G * sizeof(unsigned long long), st);
+    cudaMemsetAsync(s->abort_flag, 0, sizeof(int), st);
+    CocgParams P{};
+    P.d = d;
+    P.H = H;
+    P.G = s->G;
+    P.C = s->C;
+    P.L = s->L;
+    P.Lp = s->Lp;
+    P.R = s->R;
+    P.warp_row_begin = s->warp_row_begin;
+    P.rp = p.rp;
+    P.ci = p.ci;
+    P.diag = p.diag;
+    P.X = s->X;
+    P.Y = s->Y;
+    P.shift = s->shift;
+    P.b = s->bhat;
+    P.x = s->x;
+    P.r = s->r;
+    P.p = s->p;
+    P.q = s->q;
+    P.tol = cocg.tol_rel;
+    P.max_iter = cocg.max_iter;
+    P.sync = s->sync;
+    P.partials = s->partials;
+    P.abort_flag = s->abort_flag;
+    P.code = s->code;
+    P.iters = s->iters;
+    P.lockstep = s->lockstep;
+    void* args[] = {&P};
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cocg_kernel), dim3(s->G * s->C),
+                                                      dim3(kThreads), args, 0, st);
+    if (e != cudaSuccess) {
+      *err = std::string("cuda: cocg launch failed: ") + cudaGetErrorString(e);
+      return PS_ERR_CUDA;
+    }
+  }
+  const int tpb = 128;
+  const size_t smem = static_cast<size_t>(2) * (tpb / 32) * N * sizeof(double);
+  idft_jump_kernel<<<s->idft_blocks, tpb, smem, st>>>(d, N, H, s->d_bins, s->tw, s->conj, s->x, U_il, U_prev_il,
+                                                      s->jpart, s->maxre, s->maxim);
+  jump_finalize_kernel<<<1, 256, 0, st>>>(N, s->idft_blocks, s->idft_blocks * (tpb / 32), s->jpart, s->maxre,
+                                          s->maxim, s->jout);
+  cudaEventRecord(s->e1, st);
+  double hj[5];
+  cudaMemcpyAsync(hj, s->jout, sizeof(hj), cudaMemcpyDeviceToHost, st);
+  std::vector<int> codes(H), iters(H);
+  std::vector<int64_t> lock(s->G);
+  int abort_h = 0;
+  if (H > 0) {
+    cudaMemcpyAsync(codes.data(), s->code, H * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(iters.data(), s->iters, H * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(lock.data(), s->lockstep, s->G * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&abort_h, s->abort_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  }
+  const cudaError_t ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) {
+    *err = std::string("cuda: spectral solve failed: ") + cudaGetErrorString(ce);
+    return PS_ERR_CUDA;
+  }
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, s->e0, s->e1);
+  if (abort_h) {
+    *err = "cuda: device barrier watchdog fired in the COCG kernel";
+    return PS_ERR_WATCHDOG;
+  }
+  int rc = PS_OK;
+  for (int hh = 0; hh < H; ++hh) {
+    its_total += iters[hh];
+    max_its = std::max(max_its, iters[hh]);
+    if (codes[hh] != PS_OK && rc == PS_OK) {
+      rc = codes[hh];
+      if (rc == PS_ERR_SINGULAR_BLOCK)
+        *err = "spectral: harmonic block p = " + std::to_string(s->harmonic[hh]) + " is singular";
+      else
+        *err = "spectral: COCG did not converge for harmonic block p = " + std::to_string(s->harmonic[hh]);
+    }
+  }
+  for (int g = 0; g < s->G && H > 0; ++g) lock_total += lock[g];
+  if (rc == PS_OK) {
+    if (!std::isfinite(hj[3]) || !std::isfinite(hj[4])) {
+      rc = PS_ERR_NONFINITE;
+      *err = "spectral: harmonic solve produced non-finite values";
+    } else if (hj[4] > kImagResidualTol * std::max(1.0, hj[3])) {
+      rc = PS_ERR_CONJ_SYMMETRY;
+      *err = "spectral: conjugate symmetry violated (imaginary residue " + std::to_string(hj[4]) + ")";
+    }
+  }
+  if (jump) *jump = hj[0];
+  if (status) {
+    std::memset(status, 0, sizeof(*status));
+    status->code = rc;
+    status->failed_index = -1;
+    status->pcg_iterations = its_total;
+    status->max_pcg_iterations = max_its;
+    status->lockstep_pcg_iterations = lock_total;
+    // canonical bytes: COCG H*160*d + 20*nnz + 4(d+1) per batched
+    // iteration; DFT 8Nd + 16Hd each way; jump +8Nd
+    const double dd = static_cast<double>(d), nz = static_cast<double>(s->nnz);
+    double bytes = 0.0;
+    for (int hh = 0; hh < H; ++hh) bytes += static_cast<double>(iters[hh]) * 160.0 * dd;
+    bytes += static_cast<double>(lock_total) * (20.0 * nz + 4.0 * (dd + 1.0));
+    bytes += 2.0 * (8.0 * N * dd + 16.0 * H * dd) + 8.0 * N * dd;
+    status->algorithmic_bytes = bytes;
+    status->kernel_ms = ms;
+  }
+  return rc;
+}
+
+int dft_forward_standalone(int n, int d, const double* U, double* spec, std::string* err) {
+  if (n < 2 || n % 2 != 0) {
+    *err = "spectral: forward_dft requires an even number of blocks >= 2, got " + std::to_string(n);
+    return PS_ERR_ODD_BLOCKS;
+  }
+  const size_t total = static_cast<size_t>(n) * d;
+  std::vector<double2> hin(total);
+  for (size_t k = 0; k < total; ++k) hin[k] = make_double2(U[k], 0.0);
+  double2 *din = nullptr, *dout = nullptr, *dtw = nullptr;
+  if (dalloc(&din, total) || dalloc(&dout, total) || dalloc(&dtw, n)) {
+    *err = "cuda: allocation failed";
+    return PS_ERR_CUDA;
+  }
+  const auto tw = twiddles(n);
+  cudaMemcpy(dtw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+  cudaMemcpy(din, hin.data(), total * sizeof(double2), cudaMemcpyHostToDevice);
+  dft_generic_kernel<<<static_cast<unsigned>((total + 255) / 256), 256>>>(n, d, dtw, 0, din, dout);
+  const cudaError_t e = cudaMemcpy(spec, dout, total * sizeof(double2), cudaMemcpyDeviceToHost);
+  cudaFree(din);
+  cudaFree(dout);
+  cudaFree(dtw);
+  if (e != cudaSuccess) {
+    *err = std::string("cuda: ") + cudaGetErrorString(e);
+    return PS_ERR_CUDA;
+  }
+  return PS_OK;
+}
+
+int dft_inverse_standalone(int n, int d, const double* spec, double* U, std::string* err) {
+  if (n < 2 || n % 2 != 0) {
+    *err = "spectral: inverse_dft requires an even number of blocks >= 2, got " + std::to_string(n);
+    return PS_ERR_ODD_BLOCKS;
+  }
+  const size_t total = static_cast<size_t>(n) * d;
+  double2 *din = nullptr, *dout = nullptr, *dtw = nullptr;
+  if (dalloc(&din, total) || dalloc(&dout, total) || dalloc(&dtw, n)) {
+    *err = "cuda: allocation failed";
+    return PS_ERR_CUDA;
+  }
+  const auto tw = twiddles(n);
+  cudaMemcpy(dtw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+  cudaMemcpy(din, spec, total * sizeof(double2), cudaMemcpyHostToDevice);
+  dft_generic_kernel<<<static_cast<unsigned>((total + 255) / 256), 256>>>(n, d, dtw, 1, din, dout);
+  std::vector<double2> hout(total);
+  const cudaError_t e = cudaMemcpy(hout.data(), dout, total * sizeof(double2), cudaMemcpyDeviceToHost);
+  cudaFree(din);
+  cudaFree(dout);
+  cudaFree(dtw);
+  if (e != cudaSuccess) {
+    *err = std::string("cuda: ") + cudaGetErrorString(e);
+    return PS_ERR_CUDA;
+  }
+  double re = 0.0, im = 0.0;
+  for (size_t k = 0; k < total; ++k) {
+    re = std::max(re, std::fabs(hout[k].x));
+    im = std::max(im, std::fabs(hout[k].y));
+  }
+  if (im > kImagResidualTol * std::max(1.0, re)) {
+    *err = "spectral: conjugate symmetry violated (imaginary residue " + std::to_string(im) + ")";
+    return PS_ERR_CONJ_SYMMETRY;
+  }
+  for (size_t k = 0; k < total; ++k) U[k] = hout[k].x;
+  return PS_OK;
+}
+
+int jump_norm_device(int count, int d, const double* cur_il, const double* prev_il, int stride, double* out,
+                     cudaStream_t st) {
+  double* part = nullptr;
+  if (dalloc(&part, static_cast<size_t>(2) * count)) return PS_ERR_CUDA;
+  strided_jump_kernel<<<count, 256, 0, st>>>(count, d, stride, cur_il, prev_il, part);
+  std::vector<double> h(static_cast<size_t>(2) * count);
+  const cudaError_t e = cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(part);
+  if (e != cudaSuccess) return PS_ERR_CUDA;
+  double change = 0.0, scale = 1.0;
+  for (int n = 0; n < count; ++n) {
+    change = std::max(change, std::sqrt(h[2 * n]));
+    scale = std::max(scale, std::sqrt(h[2 * n + 1]));
+  }
+  *out = change / scale;
+  return PS_OK;
+}
+
+}  // namespace pppc

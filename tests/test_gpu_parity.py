@@ -1,0 +1,300 @@
+"""Parity of the B200 path (through the C ABI) with the CPU oracle.
+
+Every test runs the device kernels via libpppc_b200.so and compares with the
+oracle's restatement of the reference on identical seeded inputs.  Tolerances:
+1e-9 relative L2 for states/iterates (north_star), the same Newton / Parareal
+iteration counts, bitwise equality where the reference demands it.
+"""
+import numpy as np
+import pytest
+
+import paper_1905_13076_b200 as ps
+from oracle import pyoracle as po
+from helpers import NEWTON_BASELINE, random_linear_problem, rel_l2, small_polar
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def test_device_is_b200():
+    info = ps.device_info()
+    assert info["cc"] == (10, 0), info
+
+
+# ------------------------------------------------------------------ a1 curves
+def test_reluctivity_matches_oracle():
+    b2 = np.concatenate([[0.0, 1e-3, 0.5, 2.0, 5.0, 5.64, 6.0, 1e4, 1e300], np.linspace(0, 30, 301)])
+    for k1, k2, k3 in ((49.4, 1.46, 520.6), (3.8, 2.17, 396.2), (3.8, 4.0, 396.2)):
+        nu, nup = ps.reluctivity("brauer", b2, k1=k1, k2=k2, k3=k3)
+        nu_o, nup_o = po.nu("brauer", b2, k1=k1, k2=k2, k3=k3)
+        np.testing.assert_allclose(nu, nu_o, rtol=1e-14)
+        np.testing.assert_allclose(nup, nup_o, rtol=1e-14)
+    nu, _ = ps.reluctivity("brauer", [0.0], k1=49.4, k2=1.46, k3=520.6)
+    assert abs(nu[0] - 570.0) <= 570.0 * 1e-14          # proj/tests/test_problem.cpp:95
+    nu, nup = ps.reluctivity("brauer", [1e4, 1e300], k1=49.4, k2=1.46, k3=520.6)
+    assert (nu == ps.api.K_VACUUM_RELUCTIVITY).all() and (nup == 0.0).all()
+
+
+# ---------------------------------------------------- a2/a3 operator refill
+@pytest.mark.parametrize("kind", ["polar", "radial"])
+def test_assembled_operators_match_oracle(kind):
+    prob = small_polar() if kind == "polar" else ps.build_coax_cable(n_r=51)
+    prop = ps.Propagator(prob, ps.TimeMesh(4, 2, prob.period), max_batch=3)
+    orc = po.Oracle(prob)
+    U = np.stack([ps.seeded_normal(7 + k, prob.dim, 10.0 ** (-4 + k)) for k in range(3)])
+    K, J = prop.assemble(U)
+    for n in range(3):
+        assert rel_l2(K[n], orc.stiffness_at(U[n])) <= 1e-13
+        assert rel_l2(J[n], orc.newton_matrix_at(U[n])) <= 1e-13
+
+
+def test_excitation_matches_oracle():
+    prob = ps.build_polar_cable(nr=12, ntheta=16, ripple_terms=5)
+    prop = ps.Propagator(prob, ps.TimeMesh(4, 2, prob.period), max_batch=6)
+    orc = po.Oracle(prob)
+    t = np.array([0.0, 0.003, 0.005, 0.0123, 0.02, -0.031])
+    f = prop.excitation(t)
+    for n in range(len(t)):
+        assert rel_l2(f[n], orc.excitation(t[n])) <= 1e-14
+
+
+# ------------------------------------------------------------- a6 newton_step
+def test_newton_step_cable_kat():
+    """proj/tests/test_propagators.cpp:71-82: >= 2 iterations, strictly decreasing residuals."""
+    cable = ps.build_coax_cable(n_r=51)
+    r = ps.newton_step(cable, np.zeros(50), 0.005, 1e-3)
+    assert r.iterations >= 2
+    assert all(b < a for a, b in zip(r.residual_norms, r.residual_norms[1:]))
+    f = po.Oracle(cable).excitation(0.005)
+    assert r.residual_norms[-1] <= 1e-9 + 1e-8 * np.linalg.norm(f)
+    u_o, its_o, trace_o, _ = po.Oracle(cable).newton_step(np.zeros(50), 0.005, 1e-3, mode=po.ITERATIVE)
+    assert r.iterations == its_o
+    assert rel_l2(r.state, u_o) <= TOL
+
+
+def test_newton_step_linear_one_iteration():
+    rng = np.random.default_rng(17)
+    p = random_linear_problem(5, 0.02, rng)
+    u_prev = rng.uniform(-1, 1, 5)
+    r = ps.newton_step(p, u_prev, 0.007, 1e-3)
+    assert r.iterations == 1
+    u_o, its_o, _, _ = po.Oracle(p).newton_step(u_prev, 0.007, 1e-3, mode=po.ITERATIVE)
+    assert rel_l2(r.state, u_o) <= TOL
+
+
+def test_newton_step_hand_values():
+    """proj/tests/test_propagators.cpp:32-45."""
+    u = ps.coarse_step(ps.build_scalar_test(0.0, 2.0, 6.0, 50.0), np.zeros(1), 0.005, 1e-3)
+    assert abs(u[0] - 3.0) <= 3e-12
+    u = ps.coarse_step(ps.build_scalar_test(1.0, 1.0, 1.0, 0.25), np.zeros(1), 1.0, 1.0)
+    assert abs(u[0] - 0.5) <= 0.5e-12
+    r = ps.newton_step(ps.build_scalar_test(1.0, 1.0, 0.0, 50.0), np.zeros(1), 0.005, 1e-3)
+    assert r.state[0] == 0.0 and r.iterations == 1
+
+
+def test_newton_budget_exhaustion_message():
+    """proj/tests/test_propagators.cpp:84-93."""
+    p = ps.build_scalar_test(1.0, 1.0, 1.0, 50.0)
+    bad = ps.NewtonSettings(tol_abs=1e-300, tol_rel=0.0, max_iter=5, damping=0.5)
+    with pytest.raises(ps.ParasteadyError, match="did not converge"):
+        ps.newton_step(p, np.zeros(1), 0.005, 1e-3, bad)
+
+
+def test_singular_step_system_reported():
+    p = ps.PeriodicProblem.linear([[0.0]], [[0.0]], [dict(pattern=[1.0], amplitude=1.0, frequency=50.0)], 0.02)
+    with pytest.raises(ps.ParasteadyError, match="singular"):
+        ps.newton_step(p, np.zeros(1), 0.005, 1e-3)
+
+
+# ------------------------------------------------------- a7/a8 propagators
+def test_fine_batch_polar_matches_oracle():
+    prob = small_polar()
+    mesh = ps.TimeMesh(6, 4, prob.period)
+    prop = ps.Propagator(prob, mesh, NEWTON_BASELINE)
+    orc = po.Oracle(prob)
+    U0 = ps.seeded_normal(19051307, 6 * prob.dim, 1e-4).reshape(6, prob.dim)
+    F = prop.fine_propagate_batch(1, U0)
+    st = prop.last_status
+    F_o = orc.fine_propagate_batch(mesh, 1, U0, newton=NEWTON_BASELINE, mode=po.ITERATIVE)
+    for n in range(6):
+        assert rel_l2(F[n], F_o[n]) <= TOL, n
+    assert st.newton_iterations == orc.last_stats.newton_iterations
+    assert st.kernel_ms > 0 and st.algorithmic_bytes > 0
+
+
+def test_fine_batch_random_start_config2_geometry_small():
+    """BASELINE configs[1] start values N(0, 1e-3) at I0 = 2000 A on a reduced mesh."""
+    prob = ps.build_polar_cable(nr=20, ntheta=32)
+    mesh = ps.TimeMesh(100, 20, prob.period)
+    prop = ps.Propagator(prob, mesh, NEWTON_BASELINE, max_batch=4)
+    orc = po.Oracle(prob)
+    U0 = np.stack([ps.seeded_normal(19051307 + n, prob.dim, 1e-3) for n in range(1, 5)])
+    F = prop.fine_propagate_batch(1, U0)
+    F_o = orc.fine_propagate_batch(mesh, 1, U0, newton=NEWTON_BASELINE, mode=po.ITERATIVE)
+    assert max(rel_l2(F[n], F_o[n]) for n in range(4)) <= TOL
+    assert prop.last_status.newton_iterations == orc.last_stats.newton_iterations
+
+
+def test_fine_equals_coarse_bitwise_for_s1():
+    """proj/tests/test_propagators.cpp:113-125 (s = 1: identical work)."""
+    rng = np.random.default_rng(23)
+    p = random_linear_problem(4, 0.02, rng)
+    prop = ps.Propagator(p, ps.TimeMesh(5, 1, 0.02))
+    U = rng.uniform(-1, 1, size=(5, 4))
+    assert np.array_equal(prop.fine_propagate_batch(1, U), prop.coarse_propagate_batch(1, U))
+
+
+def test_batch_split_is_bitwise_invariant():
+    """Worker-count independence (proj/tests/test_engine.cpp:253-271): a
+    subinterval's result does not depend on the other members of its batch."""
+    prob = small_polar()
+    mesh = ps.TimeMesh(8, 3, prob.period)
+    prop = ps.Propagator(prob, mesh, NEWTON_BASELINE)
+    U0 = ps.seeded_normal(5, 8 * prob.dim, 1e-4).reshape(8, prob.dim)
+    full = prop.fine_propagate_batch(1, U0)
+    for n in (1, 4, 8):
+        one = prop.fine_propagate_batch(n, U0[n - 1:n])
+        assert np.array_equal(one[0], full[n - 1]), n
+    part = prop.fine_propagate_batch(3, U0[2:7])
+    assert np.array_equal(part, full[2:7])
+
+
+def test_coarse_linear_batch_matches_oracle():
+    prob = small_polar()
+    mesh = ps.TimeMesh(6, 4, prob.period)
+    lin = ps.Propagator(prob, mesh, NEWTON_BASELINE).frozen()
+    orc = po.Oracle(prob).frozen()
+    U0 = ps.seeded_normal(3, 6 * prob.dim, 1e-3).reshape(6, prob.dim)
+    G = lin.coarse_propagate_batch(1, U0)
+    G_o = orc.coarse_propagate_batch(mesh, 1, U0, mode=po.ITERATIVE)
+    assert rel_l2(G, G_o) <= TOL
+    sweep = lin.coarse_sweep()
+    sweep_o = orc.coarse_sweep(mesh, mode=po.ITERATIVE)
+    assert rel_l2(sweep, sweep_o) <= TOL
+
+
+# ------------------------------------------------------------ a10-a14 spectral
+def test_dft_known_answers():
+    """proj/tests/test_spectral.cpp:66-101."""
+    hat = ps.forward_dft(np.array([1.0, 2.0, 3.0, 4.0]).reshape(4, 1))[:, 0]
+    np.testing.assert_allclose(hat, [5.0, -1 + 1j, -1.0, -1 - 1j], atol=1e-14)
+    n = 8
+    cos = np.cos(2 * np.pi * np.arange(n) / n).reshape(n, 1)
+    hat = ps.forward_dft(cos)[:, 0]
+    assert abs(hat[1] - np.sqrt(n) / 2) <= 1e-13 and abs(hat[n - 1] - np.sqrt(n) / 2) <= 1e-13
+    rng = np.random.default_rng(37)
+    U = rng.uniform(-1, 1, size=(16, 5))
+    back = ps.inverse_dft(ps.forward_dft(U))
+    assert np.max(np.abs(back - U)) <= 1e-12
+    spec = np.zeros((4, 1), dtype=complex)
+    spec[1, 0] = 1j
+    with pytest.raises(ps.ParasteadyError, match="conjugate symmetry"):
+        ps.inverse_dft(spec)
+
+
+def test_jump_norm_values():
+    """proj/tests/test_engine.cpp:24-44."""
+    assert ps.jump_norm([[1, 0]], [[0, 0]]) == 1.0
+    assert ps.jump_norm([[0.5, 0], [0, 0]], [[0, 0], [0.25, 0]]) == 0.5
+    assert abs(ps.jump_norm([[10, 0]], [[8, 0]]) - 0.2) <= 1e-14
+    assert ps.jump_norm([[3, 4]], [[3, 4]]) == 0.0
+
+
+@pytest.mark.parametrize("conj", [True, False])
+def test_multiharmonic_matches_oracle_and_direct(conj):
+    rng = np.random.default_rng(67)
+    p = random_linear_problem(3, 0.02, rng)
+    mesh = ps.TimeMesh(8, 1, 0.02)
+    lin = ps.Propagator(p, mesh)
+    solver = ps.MultiharmonicCyclicSolver(lin, use_conjugate_symmetry=conj)
+    rhs = rng.uniform(-1, 1, size=(8, 3))
+    U = solver.solve(rhs)
+    orc = po.Oracle(p)
+    assert rel_l2(U, orc.mh_solve(mesh, rhs, use_conjugate_symmetry=conj, mode=po.ITERATIVE)) <= TOL
+    direct = orc.solve_cyclic_direct(mesh, rhs)
+    assert np.max(np.abs(U - direct)) <= 1e-10 * max(1.0, np.max(np.linalg.norm(direct, axis=1)))
+
+
+def test_multiharmonic_polar_frozen_matches_oracle():
+    prob = small_polar()
+    mesh = ps.TimeMesh(16, 2, prob.period)
+    lin = ps.Propagator(prob, mesh).frozen()
+    lin.mh_setup(True)
+    orc = po.Oracle(prob).frozen()
+    rng = np.random.default_rng(5)
+    F = rng.normal(0, 1e-3, size=(16, prob.dim))
+    G = rng.normal(0, 1e-3, size=(16, prob.dim))
+    rhs = lin.assemble_rhs(F, G)
+    rhs_o = orc.assemble_rhs(mesh, F, G)
+    assert rel_l2(rhs, rhs_o) <= 1e-13
+    U = lin.mh_solve(rhs_o)
+    U_o = orc.mh_solve(mesh, rhs_o, mode=po.ITERATIVE)
+    assert rel_l2(U, U_o) <= TOL
+    U_d = orc.mh_solve(mesh, rhs_o, mode=po.DIRECT)
+    assert rel_l2(U, U_d) <= 1e-9
+
+
+def test_odd_blocks_rejected():
+    p = ps.build_dae_pair()
+    lin = ps.Propagator(p, ps.TimeMesh(5, 3, p.period))
+    with pytest.raises(ps.ParasteadyError, match="even number of blocks"):
+        lin.mh_setup(True)
+
+
+def test_singular_harmonic_block_reported():
+    """proj/tests/test_spectral.cpp:331-354: zero stiffness -> Lambda_0 = 0."""
+    p = ps.PeriodicProblem.linear(np.eye(2), np.zeros((2, 2)),
+                                  [dict(pattern=[1.0, 1.0], amplitude=1.0, frequency=50.0)], 0.02)
+    lin = ps.Propagator(p, ps.TimeMesh(4, 1, 0.02))
+    lin.mh_setup(True)
+    rng = np.random.default_rng(3)
+    with pytest.raises(ps.ParasteadyError, match="singular"):
+        lin.mh_solve(rng.uniform(-1, 1, size=(4, 2)))
+
+
+# ------------------------------------------------------------------ a16 PP-PC
+def test_pppc_dae_pair_matches_oracle():
+    """proj/tests/test_engine.cpp:229-251 setup (N=8, s=5, tol 1e-10)."""
+    p = ps.build_dae_pair()
+    mesh = ps.TimeMesh(8, 5, p.period)
+    es = ps.EngineSettings(mesh, tol=1e-10)
+    res = ps.solve_pp_pc(p, es, keep_iterates=True)
+    U_o, hist_o, its_o = po.Oracle(p).solve_pp_pc(es, mode=po.ITERATIVE, keep_iterates=True)
+    assert res.history["converged"] and hist_o["converged"]
+    assert res.history["iterations"] == hist_o["iterations"]
+    for k in range(hist_o["iterations"]):
+        assert rel_l2(res.iterates[k], its_o[k]) <= TOL, k
+    assert ps.fine_periodicity_defect(p, res.trajectory, mesh) <= 1e-7
+
+
+def test_pppc_radial_cable_nonlinear():
+    """proj/tests/test_engine.cpp:288-315 (n_r = 41, N = 4, s = 10, tol 1e-8)."""
+    cable = ps.build_coax_cable(n_r=41)
+    mesh = ps.TimeMesh(4, 10, cable.period)
+    es = ps.EngineSettings(mesh, tol=1e-8, max_iterations=10)
+    res = ps.solve_pp_pc(cable, es, keep_iterates=True)
+    assert res.history["converged"] and res.history["iterations"] <= 10
+    U_o, hist_o, its_o = po.Oracle(cable).solve_pp_pc(es, mode=po.ITERATIVE, keep_iterates=True)
+    assert res.history["iterations"] == hist_o["iterations"]
+    for k in range(hist_o["iterations"]):
+        assert rel_l2(res.iterates[k], its_o[k]) <= TOL, k
+    assert ps.fine_periodicity_defect(cable, res.trajectory, mesh) <= 1e-5
+    j = res.history["jumps"]
+    assert all(j[k] < j[k - 1] for k in range(2, len(j)))
+
+
+@pytest.mark.slow
+def test_pppc_config1_matches_oracle():
+    """BASELINE configs[0] geometry/mesh/time grid (nr=40 x ntheta=64, N=20, s=50)
+    at the reference-convergent current I0 = 20 A."""
+    prob = ps.build_polar_cable(current=20.0)
+    mesh = ps.TimeMesh(20, 50, prob.period)
+    es = ps.EngineSettings(mesh, tol=1e-6, max_iterations=20, newton=NEWTON_BASELINE)
+    res = ps.solve_pp_pc(prob, es, keep_iterates=True)
+    U_o, hist_o, its_o = po.Oracle(prob).solve_pp_pc(es, mode=po.ITERATIVE, keep_iterates=True)
+    assert res.history["converged"] == hist_o["converged"] is True
+    assert res.history["iterations"] == hist_o["iterations"]
+    for k in range(hist_o["iterations"]):
+        assert rel_l2(res.iterates[k], its_o[k]) <= TOL, k
+    assert rel_l2(res.trajectory, U_o) <= TOL
