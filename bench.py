@@ -1,0 +1,328 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 PP-PC hot path on BASELINE.json configs[1]:
+the batched fine propagators F_n (N = 100 subintervals x s = 20 implicit-Euler
+steps, Newton + Jacobi-PCG) on the 2-D polar cable nr = 200 x ntheta = 256
+(d = 50,945), start values N(0, 1e-3) per DOF.
+
+One "step" = one batched fine propagation of all N subintervals (one launch of
+the persistent propagation kernel).  Metric: fine-propagator DOF-timesteps/s =
+N * s * d / t.  Multi-GPU: one process per GPU, each rank propagates its own
+N subintervals (weak scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fine-propagator DOF-timesteps/s"
+UNIT = "DOF-timesteps/s"
+SEED = 19051307
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--nr", type=int, default=200)
+    ap.add_argument("--ntheta", type=int, default=256)
+    ap.add_argument("--subintervals", type=int, default=100)
+    ap.add_argument("--fine-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=1)
+    ap.add_argument("--cpu-sample-systems", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload(args):
+    import numpy as np
+    import paper_1905_13076_b200 as ps
+    prob = ps.build_polar_cable(nr=args.nr, ntheta=args.ntheta)
+    mesh = ps.TimeMesh(args.subintervals, args.fine_steps, prob.period)
+    newton = ps.NewtonSettings(tol_abs=1e-6, tol_rel=1e-10, max_iter=50, line_search=30)
+    pcg = ps.KrylovSettings(tol_rel=1e-12, max_iter=50000)
+    return prob, mesh, newton, pcg
+
+
+def start_states(prob, n_sub, rank):
+    import numpy as np
+    import paper_1905_13076_b200 as ps
+    U = np.empty((n_sub, prob.dim))
+    for n in range(1, n_sub + 1):
+        U[n - 1] = ps.seeded_normal(SEED + rank * n_sub + n, prob.dim, 1e-3)
+    return U
+
+
+def config_dict(args, prob):
+    return {
+        "workload": "BASELINE configs[1]: batched fine propagators, 2-D polar P1 cable",
+        "nr": args.nr, "ntheta": args.ntheta, "dof": prob.dim, "nnz": prob.nnz,
+        "subintervals_per_gpu": args.subintervals, "fine_steps": args.fine_steps,
+        "current_A": 2000.0, "start_values": "N(0, 1e-3) per DOF, seeded",
+        "newton": "tol_rel 1e-10, tol_abs 1e-6, max 50, backtracking 30 (DESIGN.md §2)",
+        "pcg": "Jacobi, rel 1e-12", "l2": "inputs larger than L2 (states + per-system matrices > 126 MB)",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for name, v in zip(names, s[3:]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg_key):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            data = json.load(f)
+        return data.get(cfg_key)
+    except Exception:
+        return None
+
+
+def cpu_baseline(args, prob, mesh, newton, pcg, U, steps_sample=None, systems=None):
+    """The oracle (reference algorithm restated: Newton with a fresh sparse LDL^T per
+    iteration, proj/src/propagators.cpp:27-58) on all host cores, bounded sample."""
+    import numpy as np
+    import paper_1905_13076_b200 as ps
+    from oracle import pyoracle as po
+    cores = os.cpu_count() or 1
+    steps_sample = steps_sample or args.cpu_sample_steps
+    systems = systems or args.cpu_sample_systems or min(args.subintervals, cores)
+    sub_mesh = ps.TimeMesh(mesh.subintervals, steps_sample, mesh.period)
+    # same step length as the full workload: dt = T/(N s); sample = first `steps_sample`
+    # steps of `systems` subintervals (mesh with s' steps keeps dt only if s' == s), so
+    # run the full-s mesh but limit time by stepping the first steps via newton_step
+    orc = po.Oracle(prob)
+    dt = mesh.fine_dt()
+    t0 = time.perf_counter()
+    import concurrent.futures as cf
+
+    def one(n):
+        u = U[n].copy()
+        t_left = mesh.boundary(n)
+        for j in range(1, steps_sample + 1):
+            t_next = mesh.boundary(n + 1) if j == mesh.fine_steps else t_left + j * dt
+            u, _, _, _ = orc.newton_step(u, t_next, dt, newton=newton, pcg=pcg, mode=po.DIRECT)
+        return u
+
+    with cf.ThreadPoolExecutor(max_workers=cores) as ex:
+        list(ex.map(one, range(systems)))
+    el = time.perf_counter() - t0
+    del sub_mesh
+    value = systems * steps_sample * prob.dim / el
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{systems} subintervals x first {steps_sample} fine step(s) of the config, direct LDL^T "
+                      f"Newton (reference algorithm), {cores} threads, {el:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    prob, mesh, newton, pcg = workload(args)
+    U = start_states(prob, args.subintervals, 0)
+    vals = []
+    for k in range(args.warmup + args.steps):
+        cb = cpu_baseline(args, prob, mesh, newton, pcg, U)
+        if k >= args.warmup:
+            vals.append(cb["value"])
+    value = statistics.median(vals)
+    cb["value"] = value
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": args.subintervals * args.fine_steps * prob.dim / value * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(args, prob), "impl": "reference",
+            "cpu_baseline": cb, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1905_13076_b200 as ps
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+
+    prob, mesh, newton, pcg = workload(args)
+    N, s, d = args.subintervals, args.fine_steps, prob.dim
+    U_host = start_states(prob, N, rank)
+    prop = ps.Propagator(prob, mesh, newton, pcg, stream=stream.cuda_stream)
+    U_dev = torch.from_numpy(U_host).to(dev)
+    out_dev = torch.empty_like(U_dev)
+    U_pin = torch.from_numpy(U_host).pin_memory()
+    out_pin = torch.empty_like(U_pin).pin_memory()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (device-resident inputs)
+    for _ in range(args.warmup):
+        prop.fine_propagate_batch_dev(1, N, U_dev.data_ptr(), out_dev.data_ptr())
+
+    # timed: inputs resident in HBM
+    statuses = []
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(args.steps):
+                st = prop.fine_propagate_batch_dev(1, N, U_dev.data_ptr(), out_dev.data_ptr())
+                statuses.append(st.as_dict())
+            ev1.record(stream)
+        barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    launches = 3 * args.steps  # transpose in, persistent propagation kernel, transpose out
+
+    # e2e: the public host-array API, H2D of the start states and D2H of F inside
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = ps.api.lib().ps_fine_propagate_batch(
+                prop._ctx, 1, N, ps.api.C.cast(U_pin.data_ptr(), ps.api._abi.dp),
+                ps.api.C.cast(out_pin.data_ptr(), ps.api._abi.dp), None)
+            prop._check(r)
+        e1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+
+    units = world * N * s * d * args.steps
+    value = units / (ms / 1e3)
+    e2e_value = units / (ms_e2e / 1e3)
+    kernel_ms = statistics.mean(x["kernel_ms"] for x in statuses)
+    bytes_per_launch = statistics.mean(x["algorithmic_bytes"] for x in statuses)
+    achieved = bytes_per_launch / (kernel_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+    last = statuses[-1]
+    cfg = config_dict(args, prob)
+    cfg["parallelism"] = f"{world} GPU(s) x {N} subintervals each (independent fine propagators)"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": N * d * 8, "d2h_bytes_per_step": N * d * 8},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic("config2"),
+                     "kernel": "propagate_kernel<false,3> (persistent Newton + Jacobi-PCG)",
+                     "peak_source": peak_src,
+                     "bytes_per_launch": bytes_per_launch, "kernel_ms": kernel_ms},
+        "solver": {"newton_iterations": last["newton_iterations"], "pcg_iterations": last["pcg_iterations"],
+                   "lockstep_pcg_iterations": last["lockstep_pcg_iterations"],
+                   "max_pcg_per_solve": last["max_pcg_iterations"],
+                   "max_newton_per_step": last["max_newton_iterations"]},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args, prob, mesh, newton, pcg, U_host)
+        except Exception as exc:  # the baseline must never hide the GPU number
+            line["cpu_baseline"] = {"value": None, "error": str(exc)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
