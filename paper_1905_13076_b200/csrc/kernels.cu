@@ -205,31 +205,39 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
   acc[3] += r * r;
 }
 
+// q_i = (A p)_i for one row and one system, plus the phase-A dot partials
+// p.q, q.z, q.Dq (z = D r).  Regular rows (<= 8 slots) issue all column-index,
+// value and gathered-operand loads before the first FMA (memory-level
+// parallelism); long rows (the polar hub) take a plain loop.
 template <bool LINEAR>
 __device__ __forceinline__ void spmv_row(const PropParams& P, int i, int sys, double (&acc)[kNDots]) {
   const size_t st = static_cast<size_t>(P.stride);
   const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+  const int len = end - base;
   double qv = 0.0;
-  int k = base;
-  for (; k + 1 < end; k += 2) {
-    const int j0 = __ldg(P.ci + k), j1 = __ldg(P.ci + k + 1);
-    double a0, a1;
-    if (LINEAR) {
-      a0 = __ldg(P.Ash + k);
-      a1 = __ldg(P.Ash + k + 1);
-    } else {
-      a0 = P.A[static_cast<size_t>(k) * st + sys];
-      a1 = P.A[static_cast<size_t>(k + 1) * st + sys];
+  if (len <= kRegularRow) {
+    int cj[kRegularRow];
+    double av[kRegularRow], pv[kRegularRow];
+#pragma unroll
+    for (int k = 0; k < kRegularRow; ++k) cj[k] = k < len ? __ldg(P.ci + base + k) : i;
+#pragma unroll
+    for (int k = 0; k < kRegularRow; ++k) {
+      if (LINEAR)
+        av[k] = k < len ? __ldg(P.Ash + base + k) : 0.0;
+      else
+        av[k] = k < len ? P.A[static_cast<size_t>(base + k) * st + sys] : 0.0;
     }
-    const double p0 = P.p[static_cast<size_t>(j0) * st + sys];
-    const double p1 = P.p[static_cast<size_t>(j1) * st + sys];
-    qv += a0 * p0;
-    qv += a1 * p1;
-  }
-  if (k < end) {
-    const int j0 = __ldg(P.ci + k);
-    const double a0 = LINEAR ? __ldg(P.Ash + k) : P.A[static_cast<size_t>(k) * st + sys];
-    qv += a0 * P.p[static_cast<size_t>(j0) * st + sys];
+#pragma unroll
+    for (int k = 0; k < kRegularRow; ++k) pv[k] = k < len ? P.p[static_cast<size_t>(cj[k]) * st + sys] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kRegularRow; ++k)
+      if (k < len) qv += av[k] * pv[k];
+  } else {
+    for (int k = base; k < end; ++k) {
+      const int j0 = __ldg(P.ci + k);
+      const double a0 = LINEAR ? __ldg(P.Ash + k) : P.A[static_cast<size_t>(k) * st + sys];
+      qv += a0 * P.p[static_cast<size_t>(j0) * st + sys];
+    }
   }
   const size_t iv = static_cast<size_t>(i) * st + sys;
   P.q[iv] = qv;
@@ -241,23 +249,52 @@ __device__ __forceinline__ void spmv_row(const PropParams& P, int i, int sys, do
   acc[2] += qv * (di * qv);
 }
 
+// Phase B for two consecutive rows (loads of both rows issued together):
+// x += alpha p (x = alpha p on the first iteration), r -= alpha q, z = D r,
+// p = z + beta p; partials r.r and r.z.
 template <bool LINEAR>
-__device__ __forceinline__ void update_row(const PropParams& P, double* x, int i, int sys, double alpha,
-                                           double beta, bool first, double (&acc)[kNDots]) {
-  const size_t iv = static_cast<size_t>(i) * P.stride + sys;
-  const double di = LINEAR ? __ldg(P.Dsh + i) : P.Dinv[iv];
-  const double pi = P.p[iv], qi = P.q[iv];
-  double ri = P.r[iv];
+__device__ __forceinline__ void update_rows(const PropParams& P, double* x, int i, bool two, int sys, double alpha,
+                                            double beta, bool first, double (&acc)[kNDots]) {
+  const size_t st = static_cast<size_t>(P.stride);
+  const size_t iv0 = static_cast<size_t>(i) * st + sys;
+  const size_t iv1 = iv0 + st;
+  double d0, d1 = 0.0, p0, p1 = 0.0, q0, q1 = 0.0, r0, r1 = 0.0, x0 = 0.0, x1 = 0.0;
+  d0 = LINEAR ? __ldg(P.Dsh + i) : P.Dinv[iv0];
+  p0 = P.p[iv0];
+  q0 = P.q[iv0];
+  r0 = P.r[iv0];
+  if (!first) x0 = x[iv0];
+  if (two) {
+    d1 = LINEAR ? __ldg(P.Dsh + i + 1) : P.Dinv[iv1];
+    p1 = P.p[iv1];
+    q1 = P.q[iv1];
+    r1 = P.r[iv1];
+    if (!first) x1 = x[iv1];
+  }
   // x0 = 0: the first update writes alpha p (the refill leaves the previous
   // Newton update in x so a line-search backtrack can still use it)
-  x[iv] = first ? alpha * pi : x[iv] + alpha * pi;
-  ri -= alpha * qi;
-  const double zi = di * ri;
-  P.r[iv] = ri;
-  P.p[iv] = zi + beta * pi;
-  acc[0] += ri * ri;
-  acc[1] += ri * zi;
+  x[iv0] = first ? alpha * p0 : x0 + alpha * p0;
+  r0 -= alpha * q0;
+  const double z0 = d0 * r0;
+  P.r[iv0] = r0;
+  P.p[iv0] = z0 + beta * p0;
+  acc[0] += r0 * r0;
+  acc[1] += r0 * z0;
+  if (two) {
+    x[iv1] = first ? alpha * p1 : x1 + alpha * p1;
+    r1 -= alpha * q1;
+    const double z1 = d1 * r1;
+    P.r[iv1] = r1;
+    P.p[iv1] = z1 + beta * p1;
+    acc[0] += r1 * r1;
+    acc[1] += r1 * z1;
+  }
 }
+
+// Per-lane actions: one action per group-barrier interval, so every system
+// advances through its own steps, Newton iterations, backtracks and PCG
+// iterations without waiting for the other systems of its group.
+enum : int { ACT_IDLE = 0, ACT_R0, ACT_A, ACT_B, ACT_U, ACT_R, ACT_L0, ACT_LU };
 
 template <bool LINEAR, int NPE>
 __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams P) {
@@ -301,172 +338,184 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   s.upd = s.bt = s.zero_dx = false;
   s.newton_total = s.pcg_total = 0;
   s.max_nit = s.max_pit = s.last_nit = 0;
+  int act = valid ? (LINEAR ? ACT_L0 : ACT_R0) : ACT_IDLE;
+  int step = 0;
 
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
   long long lockstep = 0;
 
-  for (int step = 0; step < P.steps; ++step) {
-    const double t_now = valid ? P.t_next[static_cast<size_t>(step) * P.count + sys] : 0.0;
-    double* xs;      // solution vector of the step's linear solves
-    const double* uin = nullptr;
-    if (LINEAR) {
-      uin = (step & 1) ? P.ubuf1 : P.ubuf0;
-      xs = (step & 1) ? P.ubuf0 : P.ubuf1;
-      // L0: b = M (u/dt) + f, x = 0, r = b, p = D b (proj/src/propagators.cpp:85-94)
-      if (s.alive) {
-        const size_t st = static_cast<size_t>(P.stride);
-        const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
-        for (int i = row_begin + sub; i < row_end; i += P.R) {
-          const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
-          double mv = 0.0;
-          for (int k = base; k < end; ++k)
-            mv += __ldg(P.M + k) * (uin[static_cast<size_t>(__ldg(P.ci + k)) * st + sys] / P.dt);
-          double f = 0.0;
-          for (int t = 0; t < P.nterms; ++t) f += cf[t] * __ldg(P.pat + static_cast<size_t>(t) * P.d + i);
-          const double b = mv + f;
-          const size_t iv = static_cast<size_t>(i) * st + sys;
-          const double z = __ldg(P.Dsh + i) * b;
-          xs[iv] = 0.0;
-          P.r[iv] = b;
-          P.p[iv] = z;
-          acc[0] += b * z;
-          acc[1] += b * b;
-        }
+  while (__syncthreads_or(act != ACT_IDLE)) {
+    const double t_now = (act != ACT_IDLE) ? P.t_next[static_cast<size_t>(step) * P.count + sys] : 0.0;
+    double* xs = LINEAR ? ((step & 1) ? P.ubuf0 : P.ubuf1) : P.x;
+    // ------------------------------------------------ this lane's action
+    if (act == ACT_A) {
+      for (int i = row_begin + sub; i < row_end; i += P.R) spmv_row<LINEAR>(P, i, sys, acc);
+    } else if (act == ACT_B) {
+      const bool first = s.pit == 0;
+      if (P.R == 1) {
+        for (int i = row_begin; i < row_end; i += 2)
+          update_rows<LINEAR>(P, xs, i, i + 1 < row_end, sys, s.alpha, s.beta, first, acc);
+      } else {
+        for (int i = row_begin + sub; i < row_end; i += P.R)
+          update_rows<LINEAR>(P, xs, i, false, sys, s.alpha, s.beta, first, acc);
       }
-      if (!group_sync_reduce<kNDots, 2>(X, sh, acc, g, c, target, bar_idx)) return;
-      if (s.alive) pcg_start(s, sh.tot[0][sl], sh.tot[1][sl], P.pcg_tol);
-    } else {
-      xs = P.x;
-      s.nact = s.alive;
-      if (s.nact)
-        for (int i = row_begin + sub; i < row_end; i += P.R) refill_row<NPE>(P, sh_curves, i, sys, step, true, acc);
-      if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, target, bar_idx)) return;
-      if (s.nact) {
-        s.tol = P.newton_tol_abs + P.newton_tol_rel * sqrt(sh.tot[1][sl]);
+    } else if (act == ACT_R0 || act == ACT_R) {
+      if constexpr (!LINEAR)
+        for (int i = row_begin + sub; i < row_end; i += P.R)
+          refill_row<NPE>(P, sh_curves, i, sys, step, act == ACT_R0, acc);
+    } else if (act == ACT_U) {
+      if (!s.zero_dx)
+        for (int i = row_begin + sub; i < row_end; i += P.R) {
+          // trial u += lambda delta (propagators.cpp:46-48), or a backtrack
+          // u -= lambda delta with lambda already halved; delta must be finite
+          const size_t iv = static_cast<size_t>(i) * P.stride + sys;
+          const double dx = P.x[iv];
+          if (s.bt) {
+            P.u[iv] -= s.lambda * dx;
+          } else {
+            acc[0] += isfinite(dx) ? 0.0 : 1.0;
+            P.u[iv] += s.lambda * dx;
+          }
+        }
+    } else if (act == ACT_L0) {
+      // b = M (u/dt) + f, x = 0, r = b, p = D b (proj/src/propagators.cpp:85-94)
+      const double* uin = (step & 1) ? P.ubuf1 : P.ubuf0;
+      const size_t st = static_cast<size_t>(P.stride);
+      const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
+      for (int i = row_begin + sub; i < row_end; i += P.R) {
+        const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+        double mv = 0.0;
+        for (int k = base; k < end; ++k)
+          mv += __ldg(P.M + k) * (uin[static_cast<size_t>(__ldg(P.ci + k)) * st + sys] / P.dt);
+        double f = 0.0;
+        for (int t = 0; t < P.nterms; ++t) f += cf[t] * __ldg(P.pat + static_cast<size_t>(t) * P.d + i);
+        const double b = mv + f;
+        const size_t iv = static_cast<size_t>(i) * st + sys;
+        const double z = __ldg(P.Dsh + i) * b;
+        xs[iv] = 0.0;
+        P.r[iv] = b;
+        P.p[iv] = z;
+        acc[0] += b * z;
+        acc[1] += b * b;
+      }
+    } else if (act == ACT_LU) {
+      // the step solution must be finite (propagators.cpp:92); x0 = 0 when b = 0
+      for (int i = row_begin + sub; i < row_end; i += P.R) {
+        const size_t iv = static_cast<size_t>(i) * P.stride + sys;
+        if (s.pit == 0) xs[iv] = 0.0;
+        acc[0] += isfinite(xs[iv]) ? 0.0 : 1.0;
+      }
+    }
+    if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, target, bar_idx)) return;
+    ++lockstep;
+    const double t0v = sh.tot[0][sl], t1v = sh.tot[1][sl], t2v = sh.tot[2][sl], t3v = sh.tot[3][sl];
+    // ------------------------------------------------ this lane's transition
+    switch (act) {
+      case ACT_R0: {
+        s.nact = true;
+        s.tol = P.newton_tol_abs + P.newton_tol_rel * sqrt(t1v);
         s.nit = 1;
-        s.res_pre = sqrt(sh.tot[0][sl]);
-        pcg_start(s, sh.tot[2][sl], sh.tot[3][sl], P.pcg_tol);
-        s.upd = s.alive;
+        s.res_pre = sqrt(t0v);
+        pcg_start(s, t2v, t3v, P.pcg_tol);
+        s.upd = true;
         s.bt = false;
         s.zero_dx = !s.pact;
         s.lambda = P.damping;
         s.ls_k = 0;
+        act = s.pact ? ACT_A : ACT_U;
+        break;
       }
-    }
-
-    // Newton loop (a single pass for linear problems)
-    for (;;) {
-      // ---------------- Jacobi-PCG on the step system
-      while (__syncthreads_or(s.pact ? 1 : 0)) {
-        if (s.pact)
-          for (int i = row_begin + sub; i < row_end; i += P.R) spmv_row<LINEAR>(P, i, sys, acc);
-        if (!group_sync_reduce<kNDots, 3>(X, sh, acc, g, c, target, bar_idx)) return;
-        ++lockstep;
-        if (s.pact) {
-          const double pq = sh.tot[0][sl], qz = sh.tot[1][sl], qdq = sh.tot[2][sl];
-          if (!isfinite(pq) || pq == 0.0) {
-            lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
-          } else {
-            s.alpha = s.rho / pq;
-            const double rho_est = s.rho - 2.0 * s.alpha * qz + s.alpha * s.alpha * qdq;
-            s.beta = rho_est / s.rho;
-          }
-        }
-        if (s.pact)
-          for (int i = row_begin + sub; i < row_end; i += P.R)
-            update_row<LINEAR>(P, xs, i, sys, s.alpha, s.beta, s.pit == 0, acc);
-        if (!group_sync_reduce<kNDots, 2>(X, sh, acc, g, c, target, bar_idx)) return;
-        if (s.pact) {
-          const double rr = sh.tot[0][sl];
-          s.rho = sh.tot[1][sl];
-          s.pit += 1;
-          if (rr <= s.stop) {
-            s.pact = false;
-            s.pcg_total += s.pit;
-            s.max_pit = max(s.max_pit, s.pit);
-          } else if (!isfinite(rr)) {
-            lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
-          } else if (s.pit >= P.pcg_max) {
-            lane_fail(s, PS_ERR_PCG_MAXITER, LINEAR ? 0.0 : s.res_pre, t_now);
-          }
-        }
-      }
-
-      if (LINEAR) {
-        // LU: the step solution must be finite (propagators.cpp:92); x0 = 0 when b = 0
-        const bool act = s.alive;
-        if (act)
-          for (int i = row_begin + sub; i < row_end; i += P.R) {
-            const size_t iv = static_cast<size_t>(i) * P.stride + sys;
-            if (s.pit == 0) xs[iv] = 0.0;
-            acc[0] += isfinite(xs[iv]) ? 0.0 : 1.0;
-          }
-        if (!group_sync_reduce<kNDots, 1>(X, sh, acc, g, c, target, bar_idx)) return;
-        if (act) {
-          if (sh.tot[0][sl] > 0.0) {
-            lane_fail(s, PS_ERR_SINGULAR, 0.0, t_now);
-          } else {
-            s.newton_total += 1;
-            s.last_nit = 1;
-            s.max_nit = max(s.max_nit, 1);
-          }
+      case ACT_A: {
+        if (!isfinite(t0v) || t0v == 0.0) {
+          lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
+        } else {
+          s.alpha = s.rho / t0v;
+          const double rho_est = s.rho - 2.0 * s.alpha * t1v + s.alpha * s.alpha * t2v;
+          s.beta = rho_est / s.rho;
+          act = ACT_B;
         }
         break;
-      } else {
-        if (!__syncthreads_or(s.upd ? 1 : 0)) break;
-        // U: trial u += lambda delta (propagators.cpp:46-48), or a backtrack
-        // u -= lambda delta with lambda already halved; delta must be finite.
-        if (s.upd)
-          for (int i = row_begin + sub; i < row_end; i += P.R) {
-            const size_t iv = static_cast<size_t>(i) * P.stride + sys;
-            if (s.zero_dx) continue;
-            const double dx = P.x[iv];
-            if (s.bt) {
-              P.u[iv] -= s.lambda * dx;
-            } else {
-              acc[0] += isfinite(dx) ? 0.0 : 1.0;
-              P.u[iv] += s.lambda * dx;
-            }
-          }
-        if (!group_sync_reduce<kNDots, 1>(X, sh, acc, g, c, target, bar_idx)) return;
-        if (s.upd && !s.bt && sh.tot[0][sl] > 0.0) lane_fail(s, PS_ERR_SINGULAR, s.res_pre, t_now);
-        // R: residual at the trial state (+ refill and PCG init for the next iterate)
-        if (s.upd)
-          for (int i = row_begin + sub; i < row_end; i += P.R) refill_row<NPE>(P, sh_curves, i, sys, step, false, acc);
-        if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, target, bar_idx)) return;
-        if (s.upd) {
-          const double post = sqrt(sh.tot[0][sl]);
-          if (P.line_search > 0 && s.ls_k < P.line_search && !(post <= s.tol) &&
-              !(post <= (1.0 - 1e-4 * s.lambda) * s.res_pre)) {
-            s.lambda *= 0.5;
-            s.ls_k += 1;
-            s.bt = true;
-          } else {
-            s.upd = false;
-            s.bt = false;
-            if (writer && P.trace) P.trace[static_cast<size_t>(sys) * P.newton_max + (s.nit - 1)] = post;
-            if (!isfinite(post)) {
-              lane_fail(s, PS_ERR_NEWTON_DIVERGED, post, t_now);
-            } else if (post <= s.tol) {
-              s.nact = false;
-              s.newton_total += s.nit;
-              s.last_nit = s.nit;
-              s.max_nit = max(s.max_nit, s.nit);
-            } else if (s.nit >= P.newton_max) {
-              lane_fail(s, PS_ERR_NEWTON_MAXITER, post, t_now);
-            } else {
-              s.nit += 1;
-              s.res_pre = post;
-              pcg_start(s, sh.tot[2][sl], sh.tot[3][sl], P.pcg_tol);
-              s.upd = s.alive;
-              s.zero_dx = !s.pact;
-              s.lambda = P.damping;
-              s.ls_k = 0;
-            }
-          }
-        }
       }
+      case ACT_B: {
+        const double rr = t0v;
+        s.rho = t1v;
+        s.pit += 1;
+        if (rr <= s.stop) {
+          s.pact = false;
+          s.pcg_total += s.pit;
+          s.max_pit = max(s.max_pit, s.pit);
+          act = LINEAR ? ACT_LU : ACT_U;
+        } else if (!isfinite(rr)) {
+          lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
+        } else if (s.pit >= P.pcg_max) {
+          lane_fail(s, PS_ERR_PCG_MAXITER, LINEAR ? 0.0 : s.res_pre, t_now);
+        } else {
+          act = ACT_A;
+        }
+        break;
+      }
+      case ACT_U: {
+        if (!s.bt && t0v > 0.0)
+          lane_fail(s, PS_ERR_SINGULAR, s.res_pre, t_now);
+        else
+          act = ACT_R;
+        break;
+      }
+      case ACT_R: {
+        const double post = sqrt(t0v);
+        if (P.line_search > 0 && s.ls_k < P.line_search && !(post <= s.tol) &&
+            !(post <= (1.0 - 1e-4 * s.lambda) * s.res_pre)) {
+          s.lambda *= 0.5;
+          s.ls_k += 1;
+          s.bt = true;
+          act = ACT_U;
+          break;
+        }
+        s.bt = false;
+        if (writer && P.trace) P.trace[static_cast<size_t>(sys) * P.newton_max + (s.nit - 1)] = post;
+        if (!isfinite(post)) {
+          lane_fail(s, PS_ERR_NEWTON_DIVERGED, post, t_now);
+        } else if (post <= s.tol) {
+          s.nact = false;
+          s.newton_total += s.nit;
+          s.last_nit = s.nit;
+          s.max_nit = max(s.max_nit, s.nit);
+          ++step;
+          act = step < P.steps ? ACT_R0 : ACT_IDLE;
+        } else if (s.nit >= P.newton_max) {
+          lane_fail(s, PS_ERR_NEWTON_MAXITER, post, t_now);
+        } else {
+          s.nit += 1;
+          s.res_pre = post;
+          pcg_start(s, t2v, t3v, P.pcg_tol);
+          s.zero_dx = !s.pact;
+          s.lambda = P.damping;
+          s.ls_k = 0;
+          act = s.pact ? ACT_A : ACT_U;
+        }
+        break;
+      }
+      case ACT_L0: {
+        pcg_start(s, t0v, t1v, P.pcg_tol);
+        act = s.pact ? ACT_A : ACT_LU;
+        break;
+      }
+      case ACT_LU: {
+        if (t0v > 0.0) {
+          lane_fail(s, PS_ERR_SINGULAR, 0.0, t_now);
+        } else {
+          s.newton_total += 1;
+          s.last_nit = 1;
+          s.max_nit = max(s.max_nit, 1);
+          ++step;
+          act = step < P.steps ? ACT_L0 : ACT_IDLE;
+        }
+        break;
+      }
+      default:
+        break;
     }
+    if (!s.alive) act = ACT_IDLE;
   }
 
   if (writer) {
