@@ -29,7 +29,28 @@ thread_local std::string g_global_error;
 struct Geometry {
   int G = 0, C = 0, L = 0, Lp = 0, R = 0;
   int* warp_row_begin = nullptr;
+  int n_long = 0;
+  int* long_rows = nullptr;
+  int* long_owner = nullptr;
 };
+
+// Rows longer than kLongRow and the block whose warp ranges contain them.
+int long_rows_of(const std::vector<int>& h_rp, const std::vector<int>& ranges, std::vector<int>* rows,
+                 std::vector<int>* owner) {
+  const int d = static_cast<int>(h_rp.size()) - 1;
+  const int parts = static_cast<int>(ranges.size()) - 1;
+  rows->clear();
+  owner->clear();
+  int part = 0;
+  for (int i = 0; i < d; ++i) {
+    while (part + 1 < parts && ranges[part + 1] <= i) ++part;
+    if (h_rp[i + 1] - h_rp[i] > kLongRow) {
+      rows->push_back(i);
+      owner->push_back(part / kWarps);
+    }
+  }
+  return PS_OK;
+}
 
 // Contiguous row ranges for C blocks x kWarps warps, balanced by row cost
 // (slots + vector streams).  Depends only on the pattern, C and R.
@@ -37,7 +58,11 @@ int row_ranges(const std::vector<int>& h_rp, int C, int R, std::vector<int>* out
   const int d = static_cast<int>(h_rp.size()) - 1;
   const int parts = C * kWarps;
   std::vector<double> cum(d + 1, 0.0);
-  for (int i = 0; i < d; ++i) cum[i + 1] = cum[i] + (h_rp[i + 1] - h_rp[i]) + 4.0;
+  for (int i = 0; i < d; ++i) {
+    const int len = h_rp[i + 1] - h_rp[i];
+    // long rows are shared by all warps of the owning block
+    cum[i + 1] = cum[i] + (len > kLongRow ? len / double(kWarps) : double(len)) + 4.0;
+  }
   out->assign(parts + 1, d);
   (*out)[0] = 0;
   int row = 0;
@@ -252,12 +277,17 @@ void build_problem(ps_ctx* ctx, const ps_problem_desc* desc) {
   P.pat = upload(desc->patterns, static_cast<size_t>(P.nterms) * P.d, "excitation patterns");
 }
 
+// Work vectors use the group-blocked layout [G][d][32] (G = ceil(max_batch/32)),
+// which is also large enough to serve as interleaved [d][N] scratch.
+size_t lanes_padded(const ps_ctx* ctx) { return static_cast<size_t>((ctx->max_batch + 31) / 32) * 32; }
+
 void alloc_work(ps_ctx* ctx) {
-  const size_t n = static_cast<size_t>(ctx->P.d) * ctx->max_batch;
+  const size_t n = static_cast<size_t>(ctx->P.d) * lanes_padded(ctx);
+  const size_t nio = static_cast<size_t>(ctx->P.d) * ctx->max_batch;
   bool ok = dalloc(&ctx->u, n) && dalloc(&ctx->uprev, n) && dalloc(&ctx->x, n) && dalloc(&ctx->r, n) &&
-            dalloc(&ctx->p, n) && dalloc(&ctx->q, n) && dalloc(&ctx->io_a, n) && dalloc(&ctx->io_b, n);
+            dalloc(&ctx->p, n) && dalloc(&ctx->q, n) && dalloc(&ctx->io_a, nio) && dalloc(&ctx->io_b, nio);
   ok = ok && dalloc(&ctx->Dinv, n);
-  if (!ctx->P.linear) ok = ok && dalloc(&ctx->A, static_cast<size_t>(ctx->P.nnz) * ctx->max_batch);
+  if (!ctx->P.linear) ok = ok && dalloc(&ctx->A, static_cast<size_t>(ctx->P.nnz) * lanes_padded(ctx));
   ok = ok && dalloc(&ctx->abort_flag, 1) && dalloc(&ctx->out, ctx->max_batch) &&
        dalloc(&ctx->lockstep, (ctx->max_batch + 31) / 32 + 1);
   if (!ok) throw Failure(PS_ERR_CUDA, "cuda: out of device memory for the work vectors");
@@ -290,6 +320,11 @@ Geometry& geometry(ps_ctx* ctx, int count) {
   std::vector<int> ranges;
   row_ranges(ctx->P.h_rp, g.C, g.R, &ranges);
   g.warp_row_begin = upload(ranges.data(), ranges.size(), "row ranges");
+  std::vector<int> lrows, lowner;
+  long_rows_of(ctx->P.h_rp, ranges, &lrows, &lowner);
+  g.n_long = static_cast<int>(lrows.size());
+  g.long_rows = upload(lrows.data(), lrows.size(), "long rows");
+  g.long_owner = upload(lowner.data(), lowner.size(), "long rows");
   return ctx->geo.emplace(count, g).first->second;
 }
 
@@ -341,7 +376,7 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   if (S.newton.max_iter < 1) throw Failure(PS_ERR_BAD_ARG, "propagator: Newton needs at least one iteration");
   Geometry& geo = geometry(ctx, count);
   const bool linear_path = P.linear && !newton_mode;
-  if (!linear_path && !ctx->A && !dalloc(&ctx->A, static_cast<size_t>(P.nnz) * ctx->max_batch))
+  if (!linear_path && !ctx->A && !dalloc(&ctx->A, static_cast<size_t>(P.nnz) * lanes_padded(ctx)))
     throw Failure(PS_ERR_CUDA, "cuda: out of device memory for the step matrices");
   const int nt = std::max(1, P.nterms);
   std::vector<double> coef(static_cast<size_t>(steps) * count * nt, 0.0);
@@ -380,6 +415,9 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.Lp = geo.Lp;
   K.R = geo.R;
   K.warp_row_begin = geo.warp_row_begin;
+  K.n_long = geo.n_long;
+  K.long_rows = geo.long_rows;
+  K.long_owner = geo.long_owner;
   K.rp = P.rp;
   K.ci = P.ci;
   K.diag = P.diag;
@@ -519,15 +557,27 @@ void check_range(const ps_time_mesh& m, int n_first, int count) {
     throw Failure(PS_ERR_BAD_ARG, "propagator: subinterval index out of range");
 }
 
-// host [count][d] -> ctx->u interleaved (stride count)
+int lanes_per_group(int count) {
+  const int G = (count + 31) / 32;
+  return (count + G - 1) / G;
+}
+
+// host [count][d] -> ctx->u group-blocked (the propagation kernels' layout)
 void stage_in_host(ps_ctx* ctx, const double* U, int count) {
   const size_t n = static_cast<size_t>(count) * ctx->P.d;
   check(cudaMemcpyAsync(ctx->io_a, U, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-  launch_to_interleaved(ctx->io_a, ctx->u, count, ctx->P.d, count, ctx->stream);
+  launch_to_blocked(ctx->io_a, ctx->u, count, ctx->P.d, lanes_per_group(count), ctx->stream);
 }
 void stage_in_dev(ps_ctx* ctx, const double* dU, int count) {
-  launch_to_interleaved(dU, ctx->u, count, ctx->P.d, count, ctx->stream);
+  launch_to_blocked(dU, ctx->u, count, ctx->P.d, lanes_per_group(count), ctx->stream);
 }
+void stage_out_blocked(ps_ctx* ctx, const double* blocked, double* U, int count) {
+  const size_t n = static_cast<size_t>(count) * ctx->P.d;
+  launch_from_blocked(blocked, ctx->io_b, count, ctx->P.d, lanes_per_group(count), ctx->stream);
+  check(cudaMemcpyAsync(U, ctx->io_b, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  check(cudaStreamSynchronize(ctx->stream), "D2H");
+}
+// interleaved [d][count] -> host [count][d]
 void stage_out_host(ps_ctx* ctx, const double* il, double* U, int count) {
   const size_t n = static_cast<size_t>(count) * ctx->P.d;
   launch_from_interleaved(il, ctx->io_b, count, ctx->P.d, count, ctx->stream);
@@ -634,7 +684,11 @@ void ps_destroy(ps_ctx* ctx) {
                   ctx->coef, ctx->tnext};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  for (auto& kv : ctx->geo) cudaFree(kv.second.warp_row_begin);
+  for (auto& kv : ctx->geo) {
+    cudaFree(kv.second.warp_row_begin);
+    cudaFree(kv.second.long_rows);
+    cudaFree(kv.second.long_owner);
+  }
   for (auto& kv : ctx->step_cache) {
     cudaFree(kv.second.first);
     cudaFree(kv.second.second);
@@ -712,7 +766,7 @@ int ps_newton_step(ps_ctx* ctx, int32_t count, const double* U_prev, const doubl
       throw;
     }
     if (status) *status = st;
-    stage_out_host(ctx, res.state, U_out, count);
+    stage_out_blocked(ctx, res.state, U_out, count);
     if (iterations || residual_norms) {
       std::vector<SysOut> outs(count);
       check(cudaMemcpy(outs.data(), ctx->out, count * sizeof(SysOut), cudaMemcpyDeviceToHost), "status");
@@ -761,10 +815,10 @@ static int propagate_api(ps_ctx* ctx, int32_t n_first, int32_t count, const doub
     }
     if (status) *status = st;
     if (dev) {
-      launch_from_interleaved(res.state, U_end, count, ctx->P.d, count, ctx->stream);
+      launch_from_blocked(res.state, U_end, count, ctx->P.d, lanes_per_group(count), ctx->stream);
       check(cudaStreamSynchronize(ctx->stream), "D2D");
     } else {
-      stage_out_host(ctx, res.state, U_end, count);
+      stage_out_blocked(ctx, res.state, U_end, count);
     }
   });
 }
@@ -795,11 +849,12 @@ void coarse_sweep_il(ps_ctx* ctx, double* U_il, ps_batch_status* total) {
   const int N = ctx->mesh.subintervals, d = ctx->P.d;
   check(cudaMemsetAsync(U_il, 0, static_cast<size_t>(d) * N * sizeof(double), ctx->stream), "zero");
   for (int n = 1; n < N; ++n) {
-    copy_column(U_il, N, n - 1, ctx->u, 1, 0, d, ctx->stream);
+    // a batch of one: group 0, lane 0 of the blocked layout (row stride 32)
+    copy_column(U_il, N, n - 1, ctx->u, 32, 0, d, ctx->stream);
     std::vector<double> t(1, boundary(ctx->mesh, n));
     ps_batch_status st{};
     PropResult res = propagate(ctx, 1, 1, coarse_dt(ctx->mesh), t, false, false, &st);
-    copy_column(res.state, 1, 0, U_il, N, n, d, ctx->stream);
+    copy_column(res.state, 32, 0, U_il, N, n, d, ctx->stream);
     if (total) {
       total->pcg_iterations += st.pcg_iterations;
       total->kernel_ms += st.kernel_ms;
@@ -861,10 +916,13 @@ int ps_assemble_operators(ps_ctx* ctx, int32_t count, const double* U, double* K
       }
       return;
     }
-    stage_in_host(ctx, U, count);
+    check(cudaMemcpyAsync(ctx->io_a, U, static_cast<size_t>(count) * P.d * sizeof(double), cudaMemcpyHostToDevice,
+                          ctx->stream),
+          "H2D");
+    launch_to_interleaved(ctx->io_a, ctx->x, count, P.d, count, ctx->stream);
     double *dK = nullptr, *dJ = nullptr;
     if (!dalloc(&dK, tot) || !dalloc(&dJ, tot)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
-    launch_assemble_ops(P, count, ctx->u, dK, dJ, ctx->stream);
+    launch_assemble_ops(P, count, ctx->x, dK, dJ, ctx->stream);
     check(cudaStreamSynchronize(ctx->stream), "assemble");
     if (K_values) check(cudaMemcpy(K_values, dK, tot * sizeof(double), cudaMemcpyDeviceToHost), "K");
     if (J_values) check(cudaMemcpy(J_values, dJ, tot * sizeof(double), cudaMemcpyDeviceToHost), "J");
@@ -1053,24 +1111,30 @@ int ps_pppc_solve(ps_ctx* fine, const ps_engine_settings* settings, const double
     const size_t nd = static_cast<size_t>(N) * d;
     for (int k = 0; k < settings->max_iterations; ++k) {
       // fine batch: F_n(U_{n-1}), all N subintervals in one launch
-      check(cudaMemcpyAsync(fine->u, U, nd * sizeof(double), cudaMemcpyDeviceToDevice, st), "U->fine");
+      const int L = lanes_per_group(N);
+      launch_il_blocked(U, fine->u, d, N, N, L, true, st);
       ps_batch_status fs{};
       PropResult fr = propagate(fine, N, fine->mesh.fine_steps, fine_dt(fine->mesh), fine_times(fine->mesh, 1, N),
                                 false, false, &fs);
+      double* F_il = fine->io_a;
+      launch_il_blocked(fr.state, F_il, d, N, N, L, false, st);
+      check(cudaStreamSynchronize(st), "fine");
       h.fine_ms += fs.kernel_ms;
       h.fine_pcg_iterations += fs.pcg_iterations;
       h.newton_iterations += fs.newton_iterations;
       h.fine_bytes += fs.algorithmic_bytes;
       // coarse batch: G_n(U_{n-1}) with the frozen linear operator
-      check(cudaMemcpyAsync(coarse->u, U, nd * sizeof(double), cudaMemcpyDeviceToDevice, coarse->stream), "U->coarse");
+      launch_il_blocked(U, coarse->u, d, N, N, L, true, coarse->stream);
       std::vector<double> tc(N);
       for (int n = 0; n < N; ++n) tc[n] = boundary(fine->mesh, n + 1);
       ps_batch_status gs{};
       PropResult gr = propagate(coarse, N, 1, coarse_dt(fine->mesh), tc, false, false, &gs);
+      double* G_il = coarse->io_a;
+      launch_il_blocked(gr.state, G_il, d, N, N, L, false, coarse->stream);
       h.coarse_ms += gs.kernel_ms;
       h.coarse_pcg_iterations += gs.pcg_iterations;
       // correction: rhs = Q (F - G) + f, multiharmonic solve, jump (in place on U)
-      if (spectral_assemble_rhs(coarse->spec, coarse->P, fr.state, gr.state, nullptr, coarse->stream) != PS_OK)
+      if (spectral_assemble_rhs(coarse->spec, coarse->P, F_il, G_il, nullptr, coarse->stream) != PS_OK)
         throw Failure(PS_ERR_CUDA, "cuda: assemble_rhs failed");
       double jump = 0.0;
       ps_batch_status ss{};

@@ -1,21 +1,23 @@
 // Batched fine / coarse propagation on B200 (sm_100a), fp64.
 //
 // One persistent cooperative kernel runs a whole batch of implicit-Euler
-// propagations  (proj/src/propagators.cpp:96-115):  every time step, every
+// propagations (proj/src/propagators.cpp:96-115): every time step, every
 // Newton iteration (proj/src/propagators.cpp:27-58) and every Jacobi-PCG
 // iteration of the step solve stays on the device.  The host only sees the
 // final states and a per-system status word.
 //
-// Layout: every per-system vector is interleaved [row][system]
-// so that, for one CSR slot, the column index is read once and the values /
-// gathered operands of all systems are contiguous.  Systems are split into
-// groups of L <= 32; a warp lane holds one (row, system) pair, a group is
-// served by C blocks of 512 threads that synchronise only among themselves
-// through a monotone arrival counter (no grid-wide barrier).  Every block
-// reduces the group's dot-product partials redundantly in a fixed order, so
-// all blocks hold bit-identical per-system scalars (alpha, beta, convergence
-// flags) and take identical branches; results are deterministic and do not
-// depend on which other systems share the batch.
+// Layout: systems are split into groups of L <= 32; group g's
+// vectors are stored row-major with 32 padded lanes, element (row i, lane l)
+// at  g*d*32 + i*32 + l  (per-system matrix values: g*nnz*32 + k*32 + l).  A
+// warp lane owns one system; one CSR slot's column index is a broadcast and
+// the group's 32 lanes read one aligned 256-byte segment, and every block
+// streams a contiguous region of each array.  A group is served by C blocks of
+// 512 threads that synchronise only among themselves through a monotone
+// arrival counter (group_sync.cuh).  Every block reduces the group's
+// dot-product partials redundantly in a fixed order, so all blocks hold
+// bit-identical per-system scalars and take identical branches.  Each lane runs
+// its own state machine (one action per barrier interval), so systems never
+// wait for one another's Newton or PCG iteration counts.
 #include "group_sync.cuh"
 #include "pppc_internal.h"
 
@@ -25,6 +27,7 @@ namespace pppc {
 namespace {
 
 constexpr double kVacuumReluctivity = 1.0 / (4.0e-7 * 3.14159265358979323846);
+constexpr int kLanes = 32;  // padded lanes per group row
 
 __device__ __forceinline__ double std_min(double a, double b) { return (b < a) ? b : a; }
 
@@ -50,15 +53,13 @@ struct Lane {
   double t_fail, res_fail;
   double tol;
   int nit;
-  bool nact;
   bool pact;
   int pit;
   double rho, stop, alpha, beta;
   double res_pre;
   double lambda;   // current Newton step length (damping, halved on backtracks)
   int ls_k;        // backtracks taken in this Newton iteration
-  bool upd;        // needs an update + residual round
-  bool bt;         // the pending round is a backtrack
+  bool bt;         // the pending update round is a backtrack
   bool zero_dx;    // the step solve took 0 iterations (delta = 0)
   long long newton_total, pcg_total;
   int max_nit, max_pit, last_nit;
@@ -67,9 +68,7 @@ struct Lane {
 __device__ __forceinline__ void lane_fail(Lane& s, int code, double res, double t) {
   if (!s.alive) return;
   s.alive = false;
-  s.nact = false;
   s.pact = false;
-  s.upd = false;
   s.code = code;
   s.res_fail = res;
   s.t_fail = t;
@@ -88,14 +87,14 @@ struct Elem {
   double nu, cc;
 };
 
+// Element quantities from the state u (element (n) at u[off + n*rs]).
 template <int NPE>
-__device__ __forceinline__ void eval_elem(const PropParams& P, const ps_curve* curves, int e,
-                                          const double* u, size_t stride, int sys,
-                                          Elem<NPE>& E) {
+__device__ __forceinline__ void eval_elem(const PropParams& P, const ps_curve* curves, int e, const double* u,
+                                          size_t off, size_t rs, Elem<NPE>& E) {
 #pragma unroll
   for (int b = 0; b < NPE; ++b) {
     const int n = __ldg(P.en + e * NPE + b);
-    E.ue[b] = n >= 0 ? u[static_cast<size_t>(n) * stride + sys] : 0.0;
+    E.ue[b] = n >= 0 ? u[off + static_cast<size_t>(n) * rs] : 0.0;
   }
 #pragma unroll
   for (int k = 0; k < NPE * NPE; ++k) E.S[k] = __ldg(P.eS + static_cast<size_t>(e) * NPE * NPE + k);
@@ -115,14 +114,30 @@ __device__ __forceinline__ void eval_elem(const PropParams& P, const ps_curve* c
   E.cc = 2.0 * nup * inva;
 }
 
+// row a of S_e and g_a by selects (no dynamically indexed local arrays)
+template <int NPE>
+__device__ __forceinline__ void elem_row(const Elem<NPE>& E, int a, double& ga, double (&Sa)[NPE]) {
+  ga = E.g[0];
+#pragma unroll
+  for (int b = 0; b < NPE; ++b) Sa[b] = E.S[b];
+#pragma unroll
+  for (int aa = 1; aa < NPE; ++aa)
+    if (a == aa) {
+      ga = E.g[aa];
+#pragma unroll
+      for (int b = 0; b < NPE; ++b) Sa[b] = E.S[aa * NPE + b];
+    }
+}
+
 // Fused residual + Jacobian refill + Jacobi diagonal + PCG init for one row
 // and one system: writes A = M/dt + J(u) into the
-// fixed CSR pattern, Dinv, r = -R, p = Dinv r, x = 0.
+// fixed CSR pattern, Dinv, r = -R, p = Dinv r.  x keeps the previous Newton
+// update (a line-search backtrack still needs it); the first PCG update
+// overwrites it.  vo / ao: this lane's vector / matrix-value base offsets.
 template <int NPE>
-__device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* curves, int i,
-                                           int sys, int step, bool first, double (&acc)[kNDots]) {
-  const size_t st = static_cast<size_t>(P.stride);
-  const size_t iv = static_cast<size_t>(i) * st + sys;
+__device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* curves, int i, int sys, size_t vo,
+                                           size_t ao, int step, bool first, double (&acc)[kNDots]) {
+  const size_t iv = vo + static_cast<size_t>(i) * kLanes;
   const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
   const int len = end - base;
   const bool regular = len <= kRegularRow;
@@ -130,18 +145,18 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
 #pragma unroll
   for (int s = 0; s < kRegularRow; ++s) jv[s] = 0.0;
   if (!regular)
-    for (int k = base; k < end; ++k) P.A[static_cast<size_t>(k) * st + sys] = 0.0;
+    for (int k = base; k < end; ++k) P.A[ao + static_cast<size_t>(k) * kLanes] = 0.0;
   double ku = 0.0;
   if constexpr (NPE == 0) {
     // linear problem under newton_step semantics: J = K (proj/src/problem.cpp:141-144)
     for (int k = base; k < end; ++k) {
       const double kk = __ldg(P.Klin + k);
-      ku += kk * P.u[static_cast<size_t>(__ldg(P.ci + k)) * st + sys];
+      ku += kk * P.u[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes];
       if (regular) {
 #pragma unroll
         for (int s = 0; s < kRegularRow; ++s) jv[s] += (k - base == s) ? kk : 0.0;
       } else {
-        P.A[static_cast<size_t>(k) * st + sys] = kk;
+        P.A[ao + static_cast<size_t>(k) * kLanes] = kk;
       }
     }
   } else {
@@ -149,19 +164,20 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
     for (int q = q0; q < q1; ++q) {
       const int2 ea = __ldg(P.adj + q);
       Elem<NPE> E;
-      eval_elem<NPE>(P, curves, ea.x, P.u, st, sys, E);
-      const int a = ea.y;
-      ku += E.nu * E.g[a];
-  #pragma unroll
+      eval_elem<NPE>(P, curves, ea.x, P.u, vo, kLanes, E);
+      double ga, Sa[NPE];
+      elem_row<NPE>(E, ea.y, ga, Sa);
+      ku += E.nu * ga;
+#pragma unroll
       for (int b = 0; b < NPE; ++b) {
         const int rel = __ldg(P.adj_rel + static_cast<size_t>(q) * NPE + b);
         if (rel < 0) continue;
-        const double v = E.nu * E.S[a * NPE + b] + E.cc * (E.g[a] * E.g[b]);
+        const double v = E.nu * Sa[b] + E.cc * (ga * E.g[b]);
         if (regular) {
-  #pragma unroll
+#pragma unroll
           for (int s = 0; s < kRegularRow; ++s) jv[s] += (rel == s) ? v : 0.0;
         } else {
-          P.A[static_cast<size_t>(base + rel) * st + sys] += v;
+          P.A[ao + static_cast<size_t>(base + rel) * kLanes] += v;
         }
       }
     }
@@ -176,7 +192,7 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
   for (int k = base; k < end; ++k) {
     const double mk = __ldg(P.M + k);
     if (!first) {
-      const size_t jv2 = static_cast<size_t>(__ldg(P.ci + k)) * st + sys;
+      const size_t jv2 = vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes;
       mr += mk * ((P.u[jv2] - P.uprev[jv2]) / P.dt);
     }
     double jk;
@@ -185,10 +201,10 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
 #pragma unroll
       for (int s = 0; s < kRegularRow; ++s) jk = (k - base == s) ? jv[s] : jk;
     } else {
-      jk = P.A[static_cast<size_t>(k) * st + sys];
+      jk = P.A[ao + static_cast<size_t>(k) * kLanes];
     }
     const double av = mk / P.dt + jk;
-    P.A[static_cast<size_t>(k) * st + sys] = av;
+    P.A[ao + static_cast<size_t>(k) * kLanes] = av;
     if (k == dslot) dval = av;
   }
   const double dinv = 1.0 / dval;
@@ -205,41 +221,11 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
   acc[3] += r * r;
 }
 
-// q_i = (A p)_i for one row and one system, plus the phase-A dot partials
-// p.q, q.z, q.Dq (z = D r).  Regular rows (<= 8 slots) issue all column-index,
-// value and gathered-operand loads before the first FMA (memory-level
-// parallelism); long rows (the polar hub) take a plain loop.
+// Phase-A epilogue for one row: store q, accumulate p.q, q.z, q.Dq (z = D r).
 template <bool LINEAR>
-__device__ __forceinline__ void spmv_row(const PropParams& P, int i, int sys, double (&acc)[kNDots]) {
-  const size_t st = static_cast<size_t>(P.stride);
-  const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
-  const int len = end - base;
-  double qv = 0.0;
-  if (len <= kRegularRow) {
-    int cj[kRegularRow];
-    double av[kRegularRow], pv[kRegularRow];
-#pragma unroll
-    for (int k = 0; k < kRegularRow; ++k) cj[k] = k < len ? __ldg(P.ci + base + k) : i;
-#pragma unroll
-    for (int k = 0; k < kRegularRow; ++k) {
-      if (LINEAR)
-        av[k] = k < len ? __ldg(P.Ash + base + k) : 0.0;
-      else
-        av[k] = k < len ? P.A[static_cast<size_t>(base + k) * st + sys] : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < kRegularRow; ++k) pv[k] = k < len ? P.p[static_cast<size_t>(cj[k]) * st + sys] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kRegularRow; ++k)
-      if (k < len) qv += av[k] * pv[k];
-  } else {
-    for (int k = base; k < end; ++k) {
-      const int j0 = __ldg(P.ci + k);
-      const double a0 = LINEAR ? __ldg(P.Ash + k) : P.A[static_cast<size_t>(k) * st + sys];
-      qv += a0 * P.p[static_cast<size_t>(j0) * st + sys];
-    }
-  }
-  const size_t iv = static_cast<size_t>(i) * st + sys;
+__device__ __forceinline__ void spmv_epilogue(const PropParams& P, int i, size_t vo, double qv,
+                                              double (&acc)[kNDots]) {
+  const size_t iv = vo + static_cast<size_t>(i) * kLanes;
   P.q[iv] = qv;
   const double di = LINEAR ? __ldg(P.Dsh + i) : P.Dinv[iv];
   const double pi = P.p[iv], ri = P.r[iv];
@@ -249,62 +235,170 @@ __device__ __forceinline__ void spmv_row(const PropParams& P, int i, int sys, do
   acc[2] += qv * (di * qv);
 }
 
-// Phase B for two consecutive rows (loads of both rows issued together):
-// x += alpha p (x = alpha p on the first iteration), r -= alpha q, z = D r,
-// p = z + beta p; partials r.r and r.z.
+// Phase A over a warp's row range: q = A p with the next row's column indices
+// and matrix values prefetched while the current row's gathered operands are
+// in flight (one dependent load round per row instead of two).  Long rows are
+// skipped (spmv_long_rows); rows between kRegularRow and kLongRow slots take a
+// plain loop.
 template <bool LINEAR>
-__device__ __forceinline__ void update_rows(const PropParams& P, double* x, int i, bool two, int sys, double alpha,
-                                            double beta, bool first, double (&acc)[kNDots]) {
-  const size_t st = static_cast<size_t>(P.stride);
-  const size_t iv0 = static_cast<size_t>(i) * st + sys;
-  const size_t iv1 = iv0 + st;
-  double d0, d1 = 0.0, p0, p1 = 0.0, q0, q1 = 0.0, r0, r1 = 0.0, x0 = 0.0, x1 = 0.0;
-  d0 = LINEAR ? __ldg(P.Dsh + i) : P.Dinv[iv0];
-  p0 = P.p[iv0];
-  q0 = P.q[iv0];
-  r0 = P.r[iv0];
-  if (!first) x0 = x[iv0];
-  if (two) {
-    d1 = LINEAR ? __ldg(P.Dsh + i + 1) : P.Dinv[iv1];
-    p1 = P.p[iv1];
-    q1 = P.q[iv1];
-    r1 = P.r[iv1];
-    if (!first) x1 = x[iv1];
+__device__ __forceinline__ void spmv_range(const PropParams& P, int rb, int re, size_t vo, size_t ao,
+                                           double (&acc)[kNDots]) {
+  if (rb >= re) return;
+  int c0[kRegularRow];
+  double a0[kRegularRow];
+  int i = rb;
+  int b0 = __ldg(P.rp + i), l0 = __ldg(P.rp + i + 1) - b0;
+#pragma unroll
+  for (int k = 0; k < kRegularRow; ++k) {
+    c0[k] = k < l0 ? __ldg(P.ci + b0 + k) : i;
+    if (LINEAR)
+      a0[k] = k < l0 ? __ldg(P.Ash + b0 + k) : 0.0;
+    else
+      a0[k] = k < l0 ? P.A[ao + static_cast<size_t>(b0 + k) * kLanes] : 0.0;
   }
-  // x0 = 0: the first update writes alpha p (the refill leaves the previous
-  // Newton update in x so a line-search backtrack can still use it)
-  x[iv0] = first ? alpha * p0 : x0 + alpha * p0;
-  r0 -= alpha * q0;
-  const double z0 = d0 * r0;
-  P.r[iv0] = r0;
-  P.p[iv0] = z0 + beta * p0;
-  acc[0] += r0 * r0;
-  acc[1] += r0 * z0;
-  if (two) {
-    x[iv1] = first ? alpha * p1 : x1 + alpha * p1;
-    r1 -= alpha * q1;
-    const double z1 = d1 * r1;
-    P.r[iv1] = r1;
-    P.p[iv1] = z1 + beta * p1;
-    acc[0] += r1 * r1;
-    acc[1] += r1 * z1;
+  while (i < re) {
+    double pv[kRegularRow];
+    const bool reg = l0 <= kRegularRow;
+#pragma unroll
+    for (int k = 0; k < kRegularRow; ++k)
+      pv[k] = (reg && k < l0) ? P.p[vo + static_cast<size_t>(c0[k]) * kLanes] : 0.0;
+    // prefetch the next row's indices and values
+    const int i1 = i + 1;
+    int b1 = 0, l1 = 0;
+    int c1[kRegularRow];
+    double a1[kRegularRow];
+    if (i1 < re) {
+      b1 = __ldg(P.rp + i1);
+      l1 = __ldg(P.rp + i1 + 1) - b1;
+    }
+#pragma unroll
+    for (int k = 0; k < kRegularRow; ++k) {
+      c1[k] = k < l1 ? __ldg(P.ci + b1 + k) : i1;
+      if (LINEAR)
+        a1[k] = k < l1 ? __ldg(P.Ash + b1 + k) : 0.0;
+      else
+        a1[k] = k < l1 ? P.A[ao + static_cast<size_t>(b1 + k) * kLanes] : 0.0;
+    }
+    if (reg) {
+      double qv = 0.0;
+#pragma unroll
+      for (int k = 0; k < kRegularRow; ++k)
+        if (k < l0) qv += a0[k] * pv[k];
+      spmv_epilogue<LINEAR>(P, i, vo, qv, acc);
+    } else if (l0 <= kLongRow) {
+      double qv = 0.0;
+      for (int k = b0; k < b0 + l0; ++k) {
+        const double av = LINEAR ? __ldg(P.Ash + k) : P.A[ao + static_cast<size_t>(k) * kLanes];
+        qv += av * P.p[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes];
+      }
+      spmv_epilogue<LINEAR>(P, i, vo, qv, acc);
+    }
+    i = i1;
+    b0 = b1;
+    l0 = l1;
+#pragma unroll
+    for (int k = 0; k < kRegularRow; ++k) {
+      c0[k] = c1[k];
+      a0[k] = a1[k];
+    }
   }
 }
 
-// Per-lane actions: one action per group-barrier interval, so every system
-// advances through its own steps, Newton iterations, backtracks and PCG
-// iterations without waiting for the other systems of its group.
-enum : int { ACT_IDLE = 0, ACT_R0, ACT_A, ACT_B, ACT_U, ACT_R, ACT_L0, ACT_LU };
+// Long rows (the polar hub: ntheta+1 slots) walked serially by one lane would
+// cost ~len dependent load rounds per SpMV and hold every block of the group at
+// the next barrier.  The owning block splits the slots across its 16 warps
+// (4 slots in flight per warp), combines the warp partials in fixed order and
+// runs the row epilogue on warp 0.  All threads of the block execute this.
+template <bool LINEAR>
+__device__ __forceinline__ void spmv_long_rows(const PropParams& P, bool active, size_t vo, size_t ao, int c,
+                                               double (*lpart)[32], double (&acc)[kNDots]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = 0; j < P.n_long; ++j) {
+    if (__ldg(P.long_owner + j) != c) continue;
+    const int i = __ldg(P.long_rows + j);
+    const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+    double part = 0.0;
+    if (active) {
+      for (int k0 = base + warp; k0 < end; k0 += 4 * kWarps) {
+        double av[4], pv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u * kWarps;
+          const int cj = k < end ? __ldg(P.ci + k) : i;
+          if (LINEAR)
+            av[u] = k < end ? __ldg(P.Ash + k) : 0.0;
+          else
+            av[u] = k < end ? P.A[ao + static_cast<size_t>(k) * kLanes] : 0.0;
+          pv[u] = k < end ? P.p[vo + static_cast<size_t>(cj) * kLanes] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) part += av[u] * pv[u];
+      }
+    }
+    lpart[warp][lane] = part;
+    __syncthreads();
+    if (warp == 0 && active) {
+      double qv = 0.0;
+      for (int w = 0; w < kWarps; ++w) qv += lpart[w][lane];
+      spmv_epilogue<LINEAR>(P, i, vo, qv, acc);
+    }
+    __syncthreads();
+  }
+}
+
+// Phase B over a warp's row range, four rows per batch (all loads of a batch
+// issued together): x += alpha p (x = alpha p on the first iteration),
+// r -= alpha q, z = D r, p = z + beta p; partials r.r and r.z.
+template <bool LINEAR>
+__device__ __forceinline__ void update_range(const PropParams& P, double* x, int rb, int re, size_t vo,
+                                             double alpha, double beta, bool first, double (&acc)[kNDots]) {
+  constexpr int B = 4;
+  for (int i0 = rb; i0 < re; i0 += B) {
+    double dv[B], pv[B], qv[B], rv[B], xv[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int i = i0 + u;
+      const bool ok = i < re;
+      const size_t iv = vo + static_cast<size_t>(ok ? i : i0) * kLanes;
+      dv[u] = ok ? (LINEAR ? __ldg(P.Dsh + i) : P.Dinv[iv]) : 0.0;
+      pv[u] = ok ? P.p[iv] : 0.0;
+      qv[u] = ok ? P.q[iv] : 0.0;
+      rv[u] = ok ? P.r[iv] : 0.0;
+      xv[u] = (ok && !first) ? x[iv] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int i = i0 + u;
+      if (i >= re) break;
+      const size_t iv = vo + static_cast<size_t>(i) * kLanes;
+      x[iv] = first ? alpha * pv[u] : xv[u] + alpha * pv[u];
+      const double r = rv[u] - alpha * qv[u];
+      const double z = dv[u] * r;
+      P.r[iv] = r;
+      P.p[iv] = z + beta * pv[u];
+      acc[0] += r * r;
+      acc[1] += r * z;
+    }
+  }
+}
+
+// Per-lane actions: one action per group-barrier interval.  ACT_WAIT idles one
+// interval so that every lane's PCG phase A falls on an even interval: lanes of
+// a warp then run the same PCG phase (no A/B divergence).
+enum : int { ACT_IDLE = 0, ACT_R0, ACT_A, ACT_B, ACT_U, ACT_R, ACT_L0, ACT_LU, ACT_WAIT };
 
 template <bool LINEAR, int NPE>
 __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams P) {
   __shared__ SyncShared<kNDots> sh;
   __shared__ ps_curve sh_curves[kMaxCurves];
+  __shared__ double lpart[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x / P.C, c = blockIdx.x % P.C;
-  const int sub = lane / P.Lp, sl = lane % P.Lp;
+  const int sl = lane;
   const int sys = g * P.L + sl;
   const bool valid = (sl < P.L) && (sys < P.count);
+  const size_t vo = static_cast<size_t>(g) * P.d * kLanes + sl;
+  const size_t ao = static_cast<size_t>(g) * P.nnz * kLanes + sl;
   if (threadIdx.x < P.ncurves) sh_curves[threadIdx.x] = P.curves[threadIdx.x];
   if (threadIdx.x == 0) sh.abort = 0;
   __syncthreads();
@@ -314,12 +408,12 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   X.abort_flag = P.abort_flag;
   X.G = P.G;
   X.C = P.C;
-  X.Lp = P.Lp;
+  X.Lp = 32;
   const int row_begin = P.warp_row_begin[c * kWarps + warp];
   const int row_end = P.warp_row_begin[c * kWarps + warp + 1];
   unsigned long long target = 0;
   int bar_idx = 0;
-  const bool writer = (c == 0) && (warp == 0) && (sub == 0) && valid;
+  const bool writer = (c == 0) && (warp == 0) && valid;
 
   Lane s;
   s.alive = valid;
@@ -328,14 +422,13 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   s.res_fail = 0.0;
   s.tol = 0.0;
   s.nit = 0;
-  s.nact = false;
   s.pact = false;
   s.pit = 0;
   s.rho = s.stop = s.alpha = s.beta = 0.0;
   s.res_pre = 0.0;
   s.lambda = 1.0;
   s.ls_k = 0;
-  s.upd = s.bt = s.zero_dx = false;
+  s.bt = s.zero_dx = false;
   s.newton_total = s.pcg_total = 0;
   s.max_nit = s.max_pit = s.last_nit = 0;
   int act = valid ? (LINEAR ? ACT_L0 : ACT_R0) : ACT_IDLE;
@@ -348,27 +441,21 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     const double t_now = (act != ACT_IDLE) ? P.t_next[static_cast<size_t>(step) * P.count + sys] : 0.0;
     double* xs = LINEAR ? ((step & 1) ? P.ubuf0 : P.ubuf1) : P.x;
     // ------------------------------------------------ this lane's action
+    if (P.n_long > 0) spmv_long_rows<LINEAR>(P, act == ACT_A, vo, ao, c, lpart, acc);
     if (act == ACT_A) {
-      for (int i = row_begin + sub; i < row_end; i += P.R) spmv_row<LINEAR>(P, i, sys, acc);
+      spmv_range<LINEAR>(P, row_begin, row_end, vo, ao, acc);
     } else if (act == ACT_B) {
-      const bool first = s.pit == 0;
-      if (P.R == 1) {
-        for (int i = row_begin; i < row_end; i += 2)
-          update_rows<LINEAR>(P, xs, i, i + 1 < row_end, sys, s.alpha, s.beta, first, acc);
-      } else {
-        for (int i = row_begin + sub; i < row_end; i += P.R)
-          update_rows<LINEAR>(P, xs, i, false, sys, s.alpha, s.beta, first, acc);
-      }
+      update_range<LINEAR>(P, xs, row_begin, row_end, vo, s.alpha, s.beta, s.pit == 0, acc);
     } else if (act == ACT_R0 || act == ACT_R) {
       if constexpr (!LINEAR)
-        for (int i = row_begin + sub; i < row_end; i += P.R)
-          refill_row<NPE>(P, sh_curves, i, sys, step, act == ACT_R0, acc);
+        for (int i = row_begin; i < row_end; ++i)
+          refill_row<NPE>(P, sh_curves, i, sys, vo, ao, step, act == ACT_R0, acc);
     } else if (act == ACT_U) {
       if (!s.zero_dx)
-        for (int i = row_begin + sub; i < row_end; i += P.R) {
+        for (int i = row_begin; i < row_end; ++i) {
           // trial u += lambda delta (propagators.cpp:46-48), or a backtrack
           // u -= lambda delta with lambda already halved; delta must be finite
-          const size_t iv = static_cast<size_t>(i) * P.stride + sys;
+          const size_t iv = vo + static_cast<size_t>(i) * kLanes;
           const double dx = P.x[iv];
           if (s.bt) {
             P.u[iv] -= s.lambda * dx;
@@ -380,17 +467,16 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     } else if (act == ACT_L0) {
       // b = M (u/dt) + f, x = 0, r = b, p = D b (proj/src/propagators.cpp:85-94)
       const double* uin = (step & 1) ? P.ubuf1 : P.ubuf0;
-      const size_t st = static_cast<size_t>(P.stride);
       const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
-      for (int i = row_begin + sub; i < row_end; i += P.R) {
+      for (int i = row_begin; i < row_end; ++i) {
         const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
         double mv = 0.0;
         for (int k = base; k < end; ++k)
-          mv += __ldg(P.M + k) * (uin[static_cast<size_t>(__ldg(P.ci + k)) * st + sys] / P.dt);
+          mv += __ldg(P.M + k) * (uin[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes] / P.dt);
         double f = 0.0;
         for (int t = 0; t < P.nterms; ++t) f += cf[t] * __ldg(P.pat + static_cast<size_t>(t) * P.d + i);
         const double b = mv + f;
-        const size_t iv = static_cast<size_t>(i) * st + sys;
+        const size_t iv = vo + static_cast<size_t>(i) * kLanes;
         const double z = __ldg(P.Dsh + i) * b;
         xs[iv] = 0.0;
         P.r[iv] = b;
@@ -400,8 +486,8 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       }
     } else if (act == ACT_LU) {
       // the step solution must be finite (propagators.cpp:92); x0 = 0 when b = 0
-      for (int i = row_begin + sub; i < row_end; i += P.R) {
-        const size_t iv = static_cast<size_t>(i) * P.stride + sys;
+      for (int i = row_begin; i < row_end; ++i) {
+        const size_t iv = vo + static_cast<size_t>(i) * kLanes;
         if (s.pit == 0) xs[iv] = 0.0;
         acc[0] += isfinite(xs[iv]) ? 0.0 : 1.0;
       }
@@ -412,12 +498,10 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     // ------------------------------------------------ this lane's transition
     switch (act) {
       case ACT_R0: {
-        s.nact = true;
         s.tol = P.newton_tol_abs + P.newton_tol_rel * sqrt(t1v);
         s.nit = 1;
         s.res_pre = sqrt(t0v);
         pcg_start(s, t2v, t3v, P.pcg_tol);
-        s.upd = true;
         s.bt = false;
         s.zero_dx = !s.pact;
         s.lambda = P.damping;
@@ -476,7 +560,6 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         if (!isfinite(post)) {
           lane_fail(s, PS_ERR_NEWTON_DIVERGED, post, t_now);
         } else if (post <= s.tol) {
-          s.nact = false;
           s.newton_total += s.nit;
           s.last_nit = s.nit;
           s.max_nit = max(s.max_nit, s.nit);
@@ -512,10 +595,14 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         }
         break;
       }
+      case ACT_WAIT:
+        act = ACT_A;
+        break;
       default:
         break;
     }
     if (!s.alive) act = ACT_IDLE;
+    if (act == ACT_A && (lockstep & 1)) act = ACT_WAIT;  // phase A only on even intervals
   }
 
   if (writer) {
@@ -534,8 +621,8 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
 }
 
 // ------------------------------------------------------------ small kernels
-__global__ void transpose_kernel(const double* __restrict__ src, double* __restrict__ dst, int rows,
-                                 int cols, int ld_src, int ld_dst) {
+__global__ void transpose_kernel(const double* __restrict__ src, double* __restrict__ dst, int rows, int cols,
+                                 int ld_src, int ld_dst) {
   __shared__ double tile[32][33];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
@@ -549,9 +636,24 @@ __global__ void transpose_kernel(const double* __restrict__ src, double* __restr
   }
 }
 
+// interleaved [d][stride] <-> group-blocked [G][d][32] (L lanes used per group)
+__global__ void il_blocked_kernel(const double* __restrict__ src, double* __restrict__ dst, int d, int count,
+                                  int stride, int L, int to_blocked) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(d) * count) return;
+  const int sys = static_cast<int>(t % count), i = static_cast<int>(t / count);
+  const int g = sys / L, l = sys % L;
+  const size_t b = (static_cast<size_t>(g) * d + i) * kLanes + l;
+  const size_t il = static_cast<size_t>(i) * stride + sys;
+  if (to_blocked)
+    dst[b] = src[il];
+  else
+    dst[il] = src[b];
+}
+
 template <int NPE>
-__global__ void assemble_ops_kernel(const PropParams P, int count, const double* __restrict__ u_il,
-                                    double* K_out, double* J_out) {
+__global__ void assemble_ops_kernel(const PropParams P, int count, const double* __restrict__ u_il, double* K_out,
+                                    double* J_out) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<int64_t>(count) * P.d) return;
   const int sys = static_cast<int>(t % count), i = static_cast<int>(t / count);
@@ -565,13 +667,14 @@ __global__ void assemble_ops_kernel(const PropParams P, int count, const double*
   for (int q = P.adj_ptr[i]; q < P.adj_ptr[i + 1]; ++q) {
     const int2 ea = P.adj[q];
     Elem<NPE> E;
-    eval_elem<NPE>(P, P.curves, ea.x, u_il, static_cast<size_t>(count), sys, E);
-    const int a = ea.y;
+    eval_elem<NPE>(P, P.curves, ea.x, u_il, static_cast<size_t>(sys), static_cast<size_t>(count), E);
+    double ga, Sa[NPE];
+    elem_row<NPE>(E, ea.y, ga, Sa);
     for (int b = 0; b < NPE; ++b) {
       const int rel = P.adj_rel[static_cast<size_t>(q) * NPE + b];
       if (rel < 0) continue;
-      if (Kr) Kr[base + rel] += E.nu * E.S[a * NPE + b];
-      if (Jr) Jr[base + rel] += E.nu * E.S[a * NPE + b] + E.cc * (E.g[a] * E.g[b]);
+      if (Kr) Kr[base + rel] += E.nu * Sa[b];
+      if (Jr) Jr[base + rel] += E.nu * Sa[b] + E.cc * (ga * E.g[b]);
     }
   }
 }
@@ -658,6 +761,32 @@ void launch_from_interleaved(const double* src, double* dst, int count, int d, i
   // src [d][stride] (first count columns) -> dst [count][d]
   dim3 grid((count + 31) / 32, (d + 31) / 32);
   transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, dst, d, count, stride, d);
+}
+
+void launch_to_blocked(const double* src, double* dst, int count, int d, int L, cudaStream_t st) {
+  // src [count][d] -> group-blocked: group g's [d][32] block from rows g*L ..
+  for (int g = 0; g * L < count; ++g) {
+    const int rows = count - g * L < L ? count - g * L : L;
+    dim3 grid((d + 31) / 32, (rows + 31) / 32);
+    transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src + static_cast<size_t>(g) * L * d,
+                                                   dst + static_cast<size_t>(g) * d * kLanes, rows, d, d, kLanes);
+  }
+}
+
+void launch_from_blocked(const double* src, double* dst, int count, int d, int L, cudaStream_t st) {
+  for (int g = 0; g * L < count; ++g) {
+    const int rows = count - g * L < L ? count - g * L : L;
+    dim3 grid((rows + 31) / 32, (d + 31) / 32);
+    transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src + static_cast<size_t>(g) * d * kLanes,
+                                                   dst + static_cast<size_t>(g) * L * d, d, rows, kLanes, d);
+  }
+}
+
+void launch_il_blocked(const double* src, double* dst, int d, int count, int stride, int L, bool to_blocked,
+                       cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(d) * count;
+  il_blocked_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(src, dst, d, count, stride, L,
+                                                                                to_blocked ? 1 : 0);
 }
 
 void launch_assemble_ops(const DevProblem& p, int count, const double* u_il, double* K_out, double* J_out,

@@ -17,7 +17,8 @@ constexpr int kThreads = kWarps * 32;  // 512
 constexpr int kMaxCurves = 8;
 constexpr int kMaxTerms = 16;
 constexpr int kNDots = 4;
-constexpr int kRegularRow = 8;         // rows with <= 8 slots use register accumulators
+constexpr int kRegularRow = 7;         // rows with <= 7 slots (the P1 polar mesh) use register accumulators
+constexpr int kLongRow = 32;           // rows with > 32 slots are split across a block's warps
 
 // Per-system outcome written by block 0 of every group.
 struct SysOut {
@@ -39,6 +40,9 @@ struct PropParams {
   int count;       // systems in the batch
   int G, C, L, Lp, R;
   const int* warp_row_begin;  // [C*kWarps + 1] contiguous row ranges per (block, warp)
+  int n_long;                 // rows longer than kLongRow and the block that owns each
+  const int* long_rows;
+  const int* long_owner;
   // pattern
   const int* rp;
   const int* ci;
@@ -125,6 +129,12 @@ struct DevProblem {
 // launches (kernels.cu)
 int launch_propagate(const PropParams& prm, bool linear, int npe, cudaStream_t st, std::string* err);
 int max_coresident_blocks(bool linear, int npe, int* out);
+// host-order [count][d] <-> group-blocked [G][d][32] (L systems per group)
+void launch_to_blocked(const double* src, double* dst, int count, int d, int L, cudaStream_t st);
+void launch_from_blocked(const double* src, double* dst, int count, int d, int L, cudaStream_t st);
+// interleaved [d][stride] <-> group-blocked
+void launch_il_blocked(const double* src, double* dst, int d, int count, int stride, int L, bool to_blocked,
+                       cudaStream_t st);
 void launch_to_interleaved(const double* src, double* dst, int count, int d, int stride,
                            cudaStream_t st);
 void launch_from_interleaved(const double* src, double* dst, int count, int d, int stride,

@@ -41,6 +41,9 @@ struct CocgParams {
   int d, H;   // DOFs, solved bins (interleave stride)
   int G, C, L, Lp, R;
   const int* warp_row_begin;
+  int n_long;
+  const int* long_rows;
+  const int* long_owner;
   const int* rp;
   const int* ci;
   const int* diag;
@@ -77,6 +80,7 @@ __device__ __forceinline__ double2 lam_diag(const CocgParams& P, int i, double2 
 
 __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
   __shared__ SyncShared<kCND> sh;
+  __shared__ double2 lpart[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x / P.C, c = blockIdx.x % P.C;
   const int sub = lane / P.Lp, sl = lane % P.Lp;
@@ -132,15 +136,69 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
   }
 
   while (__syncthreads_or(s.act ? 1 : 0)) {
+    // long rows (the polar hub): slots split across the owning block's warps
+    for (int j = 0; j < P.n_long; ++j) {
+      if (__ldg(P.long_owner + j) != c) continue;
+      const int i = __ldg(P.long_rows + j);
+      const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+      double2 part = make_double2(0.0, 0.0);
+      if (s.act)
+        for (int k = base + warp; k < end; k += kWarps) {
+          const int cj = __ldg(P.ci + k);
+          const double xk = __ldg(P.X + k), yk = __ldg(P.Y + k);
+          part = cadd(part, cmul(make_double2(xk + s_b.x * yk, s_b.y * yk), P.p[static_cast<size_t>(cj) * H + h]));
+        }
+      lpart[warp][lane] = part;
+      __syncthreads();
+      if (warp == 0 && s.act) {
+        double2 qv = make_double2(0.0, 0.0);
+        for (int w = 0; w < kWarps; ++w) qv = cadd(qv, lpart[w][lane]);
+        const size_t iv = static_cast<size_t>(i) * H + h;
+        P.q[iv] = qv;
+        const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
+        const double2 pi = P.p[iv], ri = P.r[iv];
+        const double2 zi = cmul(dinv, ri);
+        const double2 pq = cmul(pi, qv), qz = cmul(qv, zi), qdq = cmul(qv, cmul(dinv, qv));
+        acc[0] += pq.x;
+        acc[1] += pq.y;
+        acc[2] += qz.x;
+        acc[3] += qz.y;
+        acc[4] += qdq.x;
+        acc[5] += qdq.y;
+      }
+      __syncthreads();
+    }
     if (s.act)
       for (int i = row_begin + sub; i < row_end; i += P.R) {
         const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+        const int len = end - base;
+        if (len > kLongRow) continue;
         double2 qv = make_double2(0.0, 0.0);
-        for (int k = base; k < end; ++k) {
-          const int j = __ldg(P.ci + k);
-          const double xv = __ldg(P.X + k), yv = __ldg(P.Y + k);
-          const double2 lam = make_double2(xv + s_b.x * yv, s_b.y * yv);
-          qv = cadd(qv, cmul(lam, P.p[static_cast<size_t>(j) * H + h]));
+        if (len <= 8) {
+          // issue every index / value / gathered-operand load before the first FMA
+          int cj[8];
+          double xv[8], yv[8];
+          double2 pv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cj[k] = k < len ? __ldg(P.ci + base + k) : i;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            xv[k] = k < len ? __ldg(P.X + base + k) : 0.0;
+            yv[k] = k < len ? __ldg(P.Y + base + k) : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            pv[k] = k < len ? P.p[static_cast<size_t>(cj[k]) * H + h] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (k < len) qv = cadd(qv, cmul(make_double2(xv[k] + s_b.x * yv[k], s_b.y * yv[k]), pv[k]));
+        } else {
+          for (int k = base; k < end; ++k) {
+            const int j = __ldg(P.ci + k);
+            const double xk = __ldg(P.X + k), yk = __ldg(P.Y + k);
+            const double2 lam = make_double2(xk + s_b.x * yk, s_b.y * yk);
+            qv = cadd(qv, cmul(lam, P.p[static_cast<size_t>(j) * H + h]));
+          }
         }
         const size_t iv = static_cast<size_t>(i) * H + h;
         P.q[iv] = qv;
@@ -437,6 +495,9 @@ struct SpectralState {
   std::vector<int> harmonic;  // signed harmonic index per solved bin
   int G = 0, C = 0, L = 0, Lp = 0, R = 0;
   int* warp_row_begin = nullptr;
+  int n_long = 0;
+  int* long_rows = nullptr;
+  int* long_owner = nullptr;
   double* X = nullptr;
   double* Y = nullptr;
   double* Q = nullptr;  // C + K for the RHS
@@ -462,6 +523,8 @@ struct SpectralState {
 
 // shared with capi.cu
 int row_ranges(const std::vector<int>& h_rp, int C, int R, std::vector<int>* out);
+int long_rows_of(const std::vector<int>& h_rp, const std::vector<int>& ranges, std::vector<int>* rows,
+                 std::vector<int>* owner);
 
 int spectral_setup(SpectralState** out, const DevProblem& p, int N, double period, int use_conj,
                    const int32_t* mask, int shift_kind, std::string* err) {
@@ -545,9 +608,8 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
     const int capacity = std::max(1, sms * per_sm);
     s->G = (s->H + 31) / 32;
     s->L = (s->H + s->G - 1) / s->G;
-    s->Lp = 1;
-    while (s->Lp < s->L) s->Lp <<= 1;
-    s->R = 32 / s->Lp;
+    s->Lp = 32;  // one lane per bin (the long-row split assumes R = 1)
+    s->R = 1;
     const int rows_min = kWarps * s->R * 4;
     s->C = std::max(1, std::min(capacity / s->G, (p.d + rows_min - 1) / rows_min));
     if (s->G > capacity) {
@@ -559,6 +621,15 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
     row_ranges(p.h_rp, s->C, s->R, &ranges);
     rc |= dalloc(&s->warp_row_begin, ranges.size());
     cudaMemcpy(s->warp_row_begin, ranges.data(), ranges.size() * sizeof(int), cudaMemcpyHostToDevice);
+    std::vector<int> lrows, lowner;
+    long_rows_of(p.h_rp, ranges, &lrows, &lowner);
+    s->n_long = static_cast<int>(lrows.size());
+    rc |= dalloc(&s->long_rows, std::max<size_t>(1, lrows.size()));
+    rc |= dalloc(&s->long_owner, std::max<size_t>(1, lrows.size()));
+    if (s->n_long) {
+      cudaMemcpy(s->long_rows, lrows.data(), lrows.size() * sizeof(int), cudaMemcpyHostToDevice);
+      cudaMemcpy(s->long_owner, lowner.data(), lowner.size() * sizeof(int), cudaMemcpyHostToDevice);
+    }
     rc |= dalloc(&s->sync, s->G);
     rc |= dalloc(&s->partials, static_cast<size_t>(2) * s->G * s->C * kCND * 32);
     rc |= dalloc(&s->abort_flag, 1);
@@ -598,7 +669,7 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
 
 void spectral_free(SpectralState* s) {
   if (!s) return;
-  void* ptrs[] = {s->warp_row_begin, s->X, s->Y, s->Q, s->shift, s->tw, s->d_bins, s->rhs, s->bhat,
+  void* ptrs[] = {s->warp_row_begin, s->long_rows, s->long_owner, s->X, s->Y, s->Q, s->shift, s->tw, s->d_bins, s->rhs, s->bhat,
                   s->x, s->r, s->p, s->q, s->sync, s->partials, s->abort_flag, s->code, s->iters,
                   s->lockstep, s->jpart, s->maxre, s->maxim, s->jout, s->coef};
   for (void* ptr : ptrs)
@@ -639,6 +710,9 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
     P.Lp = s->Lp;
     P.R = s->R;
     P.warp_row_begin = s->warp_row_begin;
+    P.n_long = s->n_long;
+    P.long_rows = s->long_rows;
+    P.long_owner = s->long_owner;
     P.rp = p.rp;
     P.ci = p.ci;
     P.diag = p.diag;
