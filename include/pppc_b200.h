@@ -274,6 +274,12 @@ int ps_pppc_solve(ps_ctx* fine_ctx, const ps_engine_settings* settings, const do
                   double* U_out, double* iterates, ps_history* history);
 int ps_fine_periodicity_defect(ps_ctx* ctx, const double* U, double* defect);
 
+/* Diagnostics: time one PCG phase of the last nonlinear propagation's batch as a
+ * standalone (ncu-replayable) kernel: mode 0 = SpMV phase (TMA-staged rows),
+ * 1 = SpMV phase (register pipeline), 2 = update phase.  bytes_out = the phase's
+ * DRAM bytes by the SURVEY.md §8d stream count. */
+int ps_phase_probe(ps_ctx* ctx, int32_t mode, int32_t reps, double* ms_out, double* bytes_out);
+
 /* --------------------------------------------------------------- builders */
 typedef struct ps_problem ps_problem;
 /* 2-D structured polar P1 cable (BASELINE.json configs). */

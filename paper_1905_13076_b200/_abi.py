@@ -178,3 +178,6 @@ def lib() -> C.CDLL:
             fn.argtypes = args
         _lib = handle
     return _lib
+
+_SIGNATURES["ps_phase_probe"] = (C.c_int, [vp, C.c_int32, C.c_int32, dp, dp])
+EXPORTED = sorted(_SIGNATURES)

@@ -7,6 +7,8 @@
 // [dim][count] layout the kernels use.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -54,14 +56,22 @@ int long_rows_of(const std::vector<int>& h_rp, const std::vector<int>& ranges, s
 
 // Contiguous row ranges for C blocks x kWarps warps, balanced by row cost
 // (slots + vector streams).  Depends only on the pattern, C and R.
-int row_ranges(const std::vector<int>& h_rp, int C, int R, std::vector<int>* out) {
+int row_ranges(const std::vector<int>& h_rp, int C, int R, std::vector<int>* out,
+               const std::vector<unsigned char>* rowkind) {
   const int d = static_cast<int>(h_rp.size()) - 1;
   const int parts = C * kWarps;
   std::vector<double> cum(d + 1, 0.0);
+  // Near-equal row counts per warp: the PCG update phase costs the same for
+  // every row and each phase ends at a group barrier, so the slowest warp sets
+  // the pace (rows of the P1 mesh differ by at most 7 vs 5 slots).  Rows with
+  // per-system values (rowkind 1) stream their values and Jacobi diagonal from
+  // HBM instead of the shared L2-resident copy and weigh 1.3 (measured phase
+  // A+B cost ratio).  Long rows are split across the owning block's warps and
+  // weigh their per-warp share.
   for (int i = 0; i < d; ++i) {
     const int len = h_rp[i + 1] - h_rp[i];
-    // long rows are shared by all warps of the owning block
-    cum[i + 1] = cum[i] + (len > kLongRow ? len / double(kWarps) : double(len)) + 4.0;
+    const double w = (rowkind && !rowkind->empty() && (*rowkind)[i]) ? 1.3 : 1.0;
+    cum[i + 1] = cum[i] + (len > kLongRow ? 1.0 + len / double(kWarps * kRegularRow) : w);
   }
   out->assign(parts + 1, d);
   (*out)[0] = 0;
@@ -111,6 +121,8 @@ struct ps_ctx {
   int spec_N = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   std::mutex mu;
+  PropParams last_params{};  // parameters of the last nonlinear propagation (phase probes)
+  bool has_last_params = false;
 };
 
 namespace {
@@ -268,6 +280,32 @@ void build_problem(ps_ctx* ctx, const ps_problem_desc* desc) {
     P.adj_ptr = upload(cnt.data(), cnt.size(), "adjacency");
     P.adj = upload(adj.data(), adj.size(), "adjacency");
     P.adj_rel = upload(rel.data(), rel.size(), "adjacency slots");
+    // Rows whose adjacent elements all have a constant reluctivity have the same
+    // step-matrix values M/dt + sum nu S_e in every system and every Newton
+    // iterate: they are read from one shared copy (h_Kc) instead of per-system
+    // values.  rowkind 1 marks rows touching a nonlinear (Brauer) element.
+    P.h_rowkind.assign(P.d, 0);
+    P.h_Kc.assign(P.nnz, 0.0);
+    for (int64_t e = 0; e < ne; ++e) {
+      const ps_curve& cv = desc->curves[desc->elem_curve[e]];
+      for (int a = 0; a < npe; ++a) {
+        const int na = desc->elem_nodes[e * npe + a];
+        if (na < 0) continue;
+        if (cv.kind != 0) {
+          P.h_rowkind[na] = 1;
+          continue;
+        }
+        for (int b = 0; b < npe; ++b) {
+          const int nb = desc->elem_nodes[e * npe + b];
+          if (nb < 0) continue;
+          const auto first = P.h_ci.begin() + P.h_rp[na], last = P.h_ci.begin() + P.h_rp[na + 1];
+          const int64_t slot = std::lower_bound(first, last, nb) - P.h_ci.begin();
+          P.h_Kc[slot] += cv.nu * desc->elem_stiff[(e * npe + a) * npe + b];
+        }
+      }
+    }
+    P.rowkind = upload(P.h_rowkind.data(), P.h_rowkind.size(), "row kinds");
+    P.Kc = upload(P.h_Kc.data(), P.h_Kc.size(), "constant stiffness");
   }
   P.nterms = desc->n_terms;
   P.period = desc->period;
@@ -318,7 +356,7 @@ Geometry& geometry(ps_ctx* ctx, int count) {
   if (g_max > ctx->capacity) throw Failure(PS_ERR_BAD_ARG, "propagator: batch too large for one cooperative launch");
   g.C = std::max(1, std::min(ctx->capacity / g_max, (ctx->P.d + rows_min - 1) / rows_min));
   std::vector<int> ranges;
-  row_ranges(ctx->P.h_rp, g.C, g.R, &ranges);
+  row_ranges(ctx->P.h_rp, g.C, g.R, &ranges, &ctx->P.h_rowkind);
   g.warp_row_begin = upload(ranges.data(), ranges.size(), "row ranges");
   std::vector<int> lrows, lowner;
   long_rows_of(ctx->P.h_rp, ranges, &lrows, &lowner);
@@ -333,7 +371,10 @@ std::pair<double*, double*> shared_step_matrix(ps_ctx* ctx, double dt) {
   if (it != ctx->step_cache.end()) return it->second;
   const DevProblem& P = ctx->P;
   std::vector<double> A(P.nnz), D(P.d);
-  for (int k = 0; k < P.nnz; ++k) A[k] = P.h_M[k] / dt + P.h_K[k];
+  // linear problems: M/dt + K; element problems: M/dt + K_const (valid on rows
+  // with rowkind 0, the only rows that read it)
+  const std::vector<double>& Kref = P.linear ? P.h_K : P.h_Kc;
+  for (int k = 0; k < P.nnz; ++k) A[k] = P.h_M[k] / dt + Kref[k];
   for (int i = 0; i < P.d; ++i) D[i] = 1.0 / A[P.h_diag[i]];
   auto pr = std::make_pair(upload(A.data(), A.size(), "step matrix"), upload(D.data(), D.size(), "jacobi"));
   return ctx->step_cache.emplace(dt, pr).first->second;
@@ -423,11 +464,16 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.diag = P.diag;
   K.M = P.M;
   K.Klin = P.K;
-  if (linear_path) {
+  K.Kc = P.Kc;
+  {
+    // shared step matrix M/dt + K (linear) or M/dt + K_const (constant-nu rows)
     const auto sm = shared_step_matrix(ctx, dt);
     K.Ash = sm.first;
     K.Dsh = sm.second;
   }
+  // rows with per-system values: every row under newton_step on a linear problem
+  // uses the shared matrix (J = K), element problems by rowkind
+  K.rowkind = P.linear ? nullptr : P.rowkind;
   K.adj_ptr = P.adj_ptr;
   K.adj = P.adj;
   K.adj_rel = P.adj_rel;
@@ -466,13 +512,52 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.out = ctx->out;
   K.trace = want_trace ? ctx->trace : nullptr;
   K.lockstep = ctx->lockstep;
+  ctx->last_params = K;
+  ctx->has_last_params = !linear_path;
 
   const int npe = P.linear ? 0 : P.npe;
+  // PPPC_DEBUG_TIMING=1: per-block work / barrier-wait timing summary on stderr
+  static const bool debug_timing = std::getenv("PPPC_DEBUG_TIMING") != nullptr;
+  unsigned long long* dbg = nullptr;
+  const int nblk = geo.G * geo.C;
+  if (debug_timing && dalloc(&dbg, static_cast<size_t>(nblk) * 9)) K.dbg = dbg;
   check(cudaEventRecord(ctx->e0, ctx->stream), "event");
   std::string err;
   const int rc = launch_propagate(K, linear_path, npe, ctx->stream, &err);
   if (rc != PS_OK) throw Failure(rc, err);
   check(cudaEventRecord(ctx->e1, ctx->stream), "event");
+  if (K.dbg) {
+    std::vector<unsigned long long> h(static_cast<size_t>(nblk) * 9);
+    check(cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream), "dbg");
+    check(cudaStreamSynchronize(ctx->stream), "dbg");
+    cudaFree(dbg);
+    const char* names[3] = {"A", "B", "other"};
+    for (int kind = 0; kind < 3; ++kind) {
+      double work = 0, wait = 0, wmin = 1e300, wmax = 0, n = 0;
+      for (int b = 0; b < nblk; ++b) {
+        const double cnt = static_cast<double>(h[b * 9 + 3 * kind + 2]);
+        if (cnt == 0) continue;
+        const double w = h[b * 9 + 3 * kind] / cnt;
+        work += h[b * 9 + 3 * kind];
+        wait += h[b * 9 + 3 * kind + 1];
+        n += cnt;
+        wmin = std::min(wmin, w);
+        wmax = std::max(wmax, w);
+      }
+      if (n > 0)
+        std::fprintf(stderr,
+                     "[pppc timing] %s: %.0f intervals/block, work %.2f us (block min %.2f max %.2f), wait %.2f us\n",
+                     names[kind], n / nblk, work / n / 1e3, wmin / 1e3, wmax / 1e3, wait / n / 1e3);
+      if (kind < 2 && std::getenv("PPPC_DEBUG_BLOCKS")) {
+        std::fprintf(stderr, "[pppc blocks %s]", names[kind]);
+        for (int b = 0; b < nblk; ++b) {
+          const double cnt = static_cast<double>(h[b * 9 + 3 * kind + 2]);
+          std::fprintf(stderr, " %.0f", cnt > 0 ? h[b * 9 + 3 * kind] / cnt / 1e3 : 0.0);
+        }
+        std::fprintf(stderr, "\n");
+      }
+    }
+  }
   std::vector<SysOut> outs(count);
   std::vector<int64_t> lock(geo.G);
   int abort_h = 0;
@@ -678,7 +763,7 @@ int ps_create(const ps_problem_desc* problem, const ps_time_mesh* mesh, const ps
 void ps_destroy(ps_ctx* ctx) {
   if (!ctx) return;
   DevProblem& P = ctx->P;
-  void* ptrs[] = {P.rp, P.ci, P.diag, P.M, P.K, P.adj_ptr, P.adj, P.adj_rel, P.en, P.eS, P.einvA, P.ecurve,
+  void* ptrs[] = {P.rowkind, P.Kc, P.rp, P.ci, P.diag, P.M, P.K, P.adj_ptr, P.adj, P.adj_rel, P.en, P.eS, P.einvA, P.ecurve,
                   P.pat, ctx->u, ctx->uprev, ctx->x, ctx->r, ctx->p, ctx->q, ctx->Dinv, ctx->A, ctx->io_a,
                   ctx->io_b, ctx->sync, ctx->partials, ctx->abort_flag, ctx->out, ctx->trace, ctx->lockstep,
                   ctx->coef, ctx->tnext};
@@ -1174,6 +1259,32 @@ int ps_pppc_solve(ps_ctx* fine, const ps_engine_settings* settings, const double
 }
 
 // fine_periodicity_defect (proj/src/engine.cpp:272-290)
+// Diagnostic: time one PCG phase of the last nonlinear propagation's batch as a
+// standalone kernel (see phase_probe_kernel).  mode 0 = phase A (TMA-staged),
+// 1 = phase A (register pipeline), 2 = phase B.  ms_out = mean over reps;
+// bytes_out = the phase's DRAM bytes by the SURVEY.md §8d stream count.
+int ps_phase_probe(ps_ctx* ctx, int32_t mode, int32_t reps, double* ms_out, double* bytes_out) {
+  if (!ctx || reps < 1) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    if (!ctx->has_last_params) throw Failure(PS_ERR_NOT_SETUP, "probe: run a nonlinear propagation first");
+    const PropParams& K = ctx->last_params;
+    double* sink = nullptr;
+    if (!dalloc(&sink, static_cast<size_t>(K.G) * K.C)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+    check(cudaEventRecord(ctx->e0, ctx->stream), "event");
+    for (int r = 0; r < reps; ++r)
+      if (launch_phase_probe(K, mode, sink, ctx->stream) != PS_OK) throw Failure(PS_ERR_CUDA, "cuda: probe launch");
+    check(cudaEventRecord(ctx->e1, ctx->stream), "event");
+    check(cudaStreamSynchronize(ctx->stream), "probe");
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, ctx->e0, ctx->e1);
+    cudaFree(sink);
+    const double d = K.d, nnz = K.nnz, nb = K.count;
+    if (ms_out) *ms_out = ms / reps;
+    if (bytes_out) *bytes_out = mode == 2 ? nb * 64.0 * d : nb * (8.0 * nnz + 40.0 * d);
+  });
+}
+
 int ps_fine_periodicity_defect(ps_ctx* ctx, const double* U, double* defect) {
   if (!ctx || !U || !defect) return PS_ERR_BAD_ARG;
   const int N = ctx->mesh.subintervals, d = ctx->P.d;

@@ -48,7 +48,7 @@ struct SyncCtx {
 // acc: this thread's partial sums (lane = system, sub-rows combined here).
 template <int NDMAX, int ND>
 __device__ bool group_sync_reduce(const SyncCtx& X, SyncShared<NDMAX>& sh, double (&acc)[NDMAX], int g, int c,
-                                  unsigned long long& target, int& bar_idx) {
+                                  unsigned long long& target, int& bar_idx, unsigned long long* t_arrive = nullptr) {
   static_assert(ND <= NDMAX, "too many dots");
   constexpr int S = SyncShared<NDMAX>::S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -71,6 +71,7 @@ __device__ bool group_sync_reduce(const SyncCtx& X, SyncShared<NDMAX>& sh, doubl
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (t_arrive) *t_arrive = globaltimer_ns();
     __threadfence();
     atomicAdd(X.sync + g, 1ull);
     target += static_cast<unsigned long long>(X.C);
@@ -100,8 +101,18 @@ __device__ bool group_sync_reduce(const SyncCtx& X, SyncShared<NDMAX>& sh, doubl
     const int k = (t / 32) % NDMAX;
     const int l = t & 31;
     if (s < S && k < ND) {
+      // issue 8 independent loads per batch before adding (fixed summation order)
       double v = 0.0;
-      for (int cc = s; cc < X.C; cc += S) v += part[static_cast<size_t>(cc) * (NDMAX * 32) + k * 32 + l];
+      for (int c0 = s; c0 < X.C; c0 += 8 * S) {
+        double tmp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int cc = c0 + u * S;
+          tmp[u] = cc < X.C ? part[static_cast<size_t>(cc) * (NDMAX * 32) + k * 32 + l] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v += tmp[u];
+      }
       sh.red[s][k][l] = v;
     }
   }

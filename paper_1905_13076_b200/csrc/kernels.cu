@@ -134,6 +134,12 @@ __device__ __forceinline__ void elem_row(const Elem<NPE>& E, int a, double& ga, 
 // fixed CSR pattern, Dinv, r = -R, p = Dinv r.  x keeps the previous Newton
 // update (a line-search backtrack still needs it); the first PCG update
 // overwrites it.  vo / ao: this lane's vector / matrix-value base offsets.
+// A row whose step-matrix values are the same for every system (linear
+// problems, and rows touching only constant-nu elements).
+__device__ __forceinline__ bool row_shared(const PropParams& P, int i) {
+  return P.rowkind == nullptr || __ldg(P.rowkind + i) == 0;
+}
+
 template <int NPE>
 __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* curves, int i, int sys, size_t vo,
                                            size_t ao, int step, bool first, double (&acc)[kNDots]) {
@@ -141,25 +147,21 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
   const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
   const int len = end - base;
   const bool regular = len <= kRegularRow;
+  const bool shared_row = row_shared(P, i);
   double jv[kRegularRow];
 #pragma unroll
   for (int s = 0; s < kRegularRow; ++s) jv[s] = 0.0;
-  if (!regular)
+  if (!regular && !shared_row)
     for (int k = base; k < end; ++k) P.A[ao + static_cast<size_t>(k) * kLanes] = 0.0;
   double ku = 0.0;
-  if constexpr (NPE == 0) {
-    // linear problem under newton_step semantics: J = K (proj/src/problem.cpp:141-144)
-    for (int k = base; k < end; ++k) {
-      const double kk = __ldg(P.Klin + k);
-      ku += kk * P.u[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes];
-      if (regular) {
-#pragma unroll
-        for (int s = 0; s < kRegularRow; ++s) jv[s] += (k - base == s) ? kk : 0.0;
-      } else {
-        P.A[ao + static_cast<size_t>(k) * kLanes] = kk;
-      }
-    }
-  } else {
+  if (shared_row) {
+    // J = K on this row (linear problems under newton_step semantics,
+    // proj/src/problem.cpp:141-144, or constant-nu elements): K u by CSR; the
+    // step-matrix values and Jacobi diagonal come from the shared copy
+    const double* Kr = NPE == 0 ? P.Klin : P.Kc;
+    for (int k = base; k < end; ++k)
+      ku += __ldg(Kr + k) * P.u[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes];
+  } else if constexpr (NPE > 0) {
     const int q0 = __ldg(P.adj_ptr + i), q1 = __ldg(P.adj_ptr + i + 1);
     for (int q = q0; q < q1; ++q) {
       const int2 ea = __ldg(P.adj + q);
@@ -195,6 +197,7 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
       const size_t jv2 = vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes;
       mr += mk * ((P.u[jv2] - P.uprev[jv2]) / P.dt);
     }
+    if (shared_row) continue;
     double jk;
     if (regular) {
       jk = 0.0;
@@ -207,11 +210,11 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
     P.A[ao + static_cast<size_t>(k) * kLanes] = av;
     if (k == dslot) dval = av;
   }
-  const double dinv = 1.0 / dval;
+  const double dinv = shared_row ? __ldg(P.Dsh + i) : 1.0 / dval;
   const double R = mr + ku - f;
   const double r = -R;
   const double z = dinv * r;
-  P.Dinv[iv] = dinv;
+  if (!shared_row) P.Dinv[iv] = dinv;
   P.r[iv] = r;
   P.p[iv] = z;
   if (first) P.uprev[iv] = P.u[iv];
@@ -222,17 +225,144 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
 }
 
 // Phase-A epilogue for one row: store q, accumulate p.q, q.z, q.Dq (z = D r).
-template <bool LINEAR>
-__device__ __forceinline__ void spmv_epilogue(const PropParams& P, int i, size_t vo, double qv,
+__device__ __forceinline__ void spmv_epilogue(const PropParams& P, int i, size_t vo, double qv, bool sh,
                                               double (&acc)[kNDots]) {
   const size_t iv = vo + static_cast<size_t>(i) * kLanes;
   P.q[iv] = qv;
-  const double di = LINEAR ? __ldg(P.Dsh + i) : P.Dinv[iv];
+  const double di = sh ? __ldg(P.Dsh + i) : P.Dinv[iv];
   const double pi = P.p[iv], ri = P.r[iv];
   const double zi = di * ri;
   acc[0] += pi * qv;
   acc[1] += qv * zi;
   acc[2] += qv * (di * qv);
+}
+
+// ---------------------------------------------------------------------------
+// TMA staging of CSR rows (nonlinear path, phase A).  Per warp, kStages
+// shared-memory stages each hold one row's per-system matrix values (up to
+// kStageSlots slots x 32 lanes), r and Dinv, filled by cp.async.bulk and
+// completed through an mbarrier (expect_tx).  One lane issues the copies
+// kStages rows ahead, so ~4 rows x 2.3 KB per warp are in flight without
+// holding registers; the lanes then read their values from shared memory.
+constexpr int kStages = 4;
+constexpr int kStageSlots = 8;
+struct StageBuf {
+  double a[kStageSlots][kLanes];
+  double r[kLanes];
+  double d[kLanes];
+};
+constexpr size_t kStageSmem = sizeof(StageBuf) * kStages * kWarps + sizeof(unsigned long long) * kStages * kWarps;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// bounded: a staging protocol error traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned long long spins = 0;
+  while (!mbar_try_wait(bar, parity))
+    if (++spins > (1ull << 28)) __trap();
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// generic-proxy global writes (made visible by the group barrier) must be
+// ordered before the async-proxy (TMA) reads of the same data
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// One lane: stage row i (values of this group's 32 lanes, r, Dinv) into `b`.
+__device__ __forceinline__ void stage_row(const PropParams& P, int i, size_t gvb, size_t gab, StageBuf* b,
+                                          unsigned long long* bar) {
+  const int base = __ldg(P.rp + i), len = __ldg(P.rp + i + 1) - base;
+  if (len > kStageSlots) {  // long / irregular rows are read directly
+    mbar_expect_tx(bar, 0);
+    return;
+  }
+  const unsigned row_bytes = kLanes * sizeof(double);
+  mbar_expect_tx(bar, (len + 2) * row_bytes);
+  tma_load(&b->a[0][0], P.A + gab + static_cast<size_t>(base) * kLanes, len * row_bytes, bar);
+  tma_load(b->r, P.r + gvb + static_cast<size_t>(i) * kLanes, row_bytes, bar);
+  tma_load(b->d, P.Dinv + gvb + static_cast<size_t>(i) * kLanes, row_bytes, bar);
+}
+
+// Phase A with TMA-staged rows (nonlinear path).  Executed by every lane of a
+// warp that has any lane in phase A; `active` lanes compute.
+__device__ __forceinline__ void spmv_range_staged(const PropParams& P, int rb, int re, int stride, size_t vo,
+                                                  size_t ao, bool active, StageBuf* bufs, unsigned long long* bars,
+                                                  unsigned& cnt, unsigned& phases, double (&acc)[kNDots]) {
+  const int lane = threadIdx.x & 31;
+  const size_t gvb = vo - lane, gab = ao - lane;
+  const int n = rb < re ? (re - rb + stride - 1) / stride : 0;
+  if (lane == 0) fence_proxy_async_global();
+  for (int j = 0; j < kStages && j < n; ++j)
+    if (lane == 0) {
+      const unsigned s = (cnt + j) % kStages;
+      stage_row(P, rb + j * stride, gvb, gab, bufs + s, bars + s);
+    }
+  for (int j = 0; j < n; ++j) {
+    const int i = rb + j * stride;
+    const unsigned s = cnt % kStages;
+    const int base = __ldg(P.rp + i), len = __ldg(P.rp + i + 1) - base;
+    int cj[kStageSlots];
+#pragma unroll
+    for (int k = 0; k < kStageSlots; ++k) cj[k] = k < len ? __ldg(P.ci + base + k) : i;
+    mbar_wait(bars + s, (phases >> s) & 1u);
+    phases ^= 1u << s;
+    if (active && len <= kStageSlots) {
+      const StageBuf* b = bufs + s;
+      double pv[kStageSlots];
+#pragma unroll
+      for (int k = 0; k < kStageSlots; ++k) pv[k] = k < len ? P.p[vo + static_cast<size_t>(cj[k]) * kLanes] : 0.0;
+      double qv = 0.0;
+#pragma unroll
+      for (int k = 0; k < kStageSlots; ++k)
+        if (k < len) qv += b->a[k][lane] * pv[k];
+      const size_t iv = vo + static_cast<size_t>(i) * kLanes;
+      P.q[iv] = qv;
+      const double di = b->d[lane], ri = b->r[lane];
+      const double pi = P.p[iv];
+      const double zi = di * ri;
+      acc[0] += pi * qv;
+      acc[1] += qv * zi;
+      acc[2] += qv * (di * qv);
+    } else if (active && len <= kLongRow) {
+      double qv = 0.0;
+      for (int k = base; k < base + len; ++k)
+        qv += P.A[ao + static_cast<size_t>(k) * kLanes] * P.p[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes];
+      const size_t iv = vo + static_cast<size_t>(i) * kLanes;
+      P.q[iv] = qv;
+      const double di = P.Dinv[iv], pi = P.p[iv], ri = P.r[iv];
+      const double zi = di * ri;
+      acc[0] += pi * qv;
+      acc[1] += qv * zi;
+      acc[2] += qv * (di * qv);
+    }
+    __syncwarp();
+    if (lane == 0 && j + kStages < n) stage_row(P, rb + (j + kStages) * stride, gvb, gab, bufs + s, bars + s);
+    ++cnt;
+  }
 }
 
 // Phase A over a warp's row range: q = A p with the next row's column indices
@@ -241,20 +371,27 @@ __device__ __forceinline__ void spmv_epilogue(const PropParams& P, int i, size_t
 // skipped (spmv_long_rows); rows between kRegularRow and kLongRow slots take a
 // plain loop.
 template <bool LINEAR>
-__device__ __forceinline__ void spmv_range(const PropParams& P, int rb, int re, size_t vo, size_t ao,
+__device__ __forceinline__ void spmv_range(const PropParams& P, int rb, int re, int stride, size_t vo, size_t ao,
                                            double (&acc)[kNDots]) {
   if (rb >= re) return;
+  (void)sizeof(LINEAR);
   int c0[kRegularRow];
   double a0[kRegularRow];
   int i = rb;
   int b0 = __ldg(P.rp + i), l0 = __ldg(P.rp + i + 1) - b0;
+  bool s0 = row_shared(P, i);
+  // own-row operands of the epilogue (p_i, r_i, Dinv_i), prefetched with the row
+  double po0, ro0, do0;
+  {
+    const size_t iv = vo + static_cast<size_t>(i) * kLanes;
+    po0 = P.p[iv];
+    ro0 = P.r[iv];
+    do0 = s0 ? __ldg(P.Dsh + i) : P.Dinv[iv];
+  }
 #pragma unroll
   for (int k = 0; k < kRegularRow; ++k) {
     c0[k] = k < l0 ? __ldg(P.ci + b0 + k) : i;
-    if (LINEAR)
-      a0[k] = k < l0 ? __ldg(P.Ash + b0 + k) : 0.0;
-    else
-      a0[k] = k < l0 ? P.A[ao + static_cast<size_t>(b0 + k) * kLanes] : 0.0;
+    a0[k] = k < l0 ? (s0 ? __ldg(P.Ash + b0 + k) : P.A[ao + static_cast<size_t>(b0 + k) * kLanes]) : 0.0;
   }
   while (i < re) {
     double pv[kRegularRow];
@@ -262,40 +399,52 @@ __device__ __forceinline__ void spmv_range(const PropParams& P, int rb, int re, 
 #pragma unroll
     for (int k = 0; k < kRegularRow; ++k)
       pv[k] = (reg && k < l0) ? P.p[vo + static_cast<size_t>(c0[k]) * kLanes] : 0.0;
-    // prefetch the next row's indices and values
-    const int i1 = i + 1;
+    // prefetch the next row's indices, values and own-row operands
+    const int i1 = i + stride;
     int b1 = 0, l1 = 0;
+    bool s1 = true;
     int c1[kRegularRow];
     double a1[kRegularRow];
+    double po1 = 0.0, ro1 = 0.0, do1 = 0.0;
     if (i1 < re) {
       b1 = __ldg(P.rp + i1);
       l1 = __ldg(P.rp + i1 + 1) - b1;
+      s1 = row_shared(P, i1);
+      const size_t iv1 = vo + static_cast<size_t>(i1) * kLanes;
+      po1 = P.p[iv1];
+      ro1 = P.r[iv1];
+      do1 = s1 ? __ldg(P.Dsh + i1) : P.Dinv[iv1];
     }
 #pragma unroll
     for (int k = 0; k < kRegularRow; ++k) {
       c1[k] = k < l1 ? __ldg(P.ci + b1 + k) : i1;
-      if (LINEAR)
-        a1[k] = k < l1 ? __ldg(P.Ash + b1 + k) : 0.0;
-      else
-        a1[k] = k < l1 ? P.A[ao + static_cast<size_t>(b1 + k) * kLanes] : 0.0;
+      a1[k] = k < l1 ? (s1 ? __ldg(P.Ash + b1 + k) : P.A[ao + static_cast<size_t>(b1 + k) * kLanes]) : 0.0;
     }
     if (reg) {
       double qv = 0.0;
 #pragma unroll
       for (int k = 0; k < kRegularRow; ++k)
         if (k < l0) qv += a0[k] * pv[k];
-      spmv_epilogue<LINEAR>(P, i, vo, qv, acc);
+      P.q[vo + static_cast<size_t>(i) * kLanes] = qv;
+      const double zi = do0 * ro0;
+      acc[0] += po0 * qv;
+      acc[1] += qv * zi;
+      acc[2] += qv * (do0 * qv);
     } else if (l0 <= kLongRow) {
       double qv = 0.0;
       for (int k = b0; k < b0 + l0; ++k) {
-        const double av = LINEAR ? __ldg(P.Ash + k) : P.A[ao + static_cast<size_t>(k) * kLanes];
+        const double av = s0 ? __ldg(P.Ash + k) : P.A[ao + static_cast<size_t>(k) * kLanes];
         qv += av * P.p[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes];
       }
-      spmv_epilogue<LINEAR>(P, i, vo, qv, acc);
+      spmv_epilogue(P, i, vo, qv, s0, acc);
     }
     i = i1;
     b0 = b1;
     l0 = l1;
+    s0 = s1;
+    po0 = po1;
+    ro0 = ro1;
+    do0 = do1;
 #pragma unroll
     for (int k = 0; k < kRegularRow; ++k) {
       c0[k] = c1[k];
@@ -317,6 +466,7 @@ __device__ __forceinline__ void spmv_long_rows(const PropParams& P, bool active,
     if (__ldg(P.long_owner + j) != c) continue;
     const int i = __ldg(P.long_rows + j);
     const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+    const bool sh = row_shared(P, i);
     double part = 0.0;
     if (active) {
       for (int k0 = base + warp; k0 < end; k0 += 4 * kWarps) {
@@ -325,10 +475,7 @@ __device__ __forceinline__ void spmv_long_rows(const PropParams& P, bool active,
         for (int u = 0; u < 4; ++u) {
           const int k = k0 + u * kWarps;
           const int cj = k < end ? __ldg(P.ci + k) : i;
-          if (LINEAR)
-            av[u] = k < end ? __ldg(P.Ash + k) : 0.0;
-          else
-            av[u] = k < end ? P.A[ao + static_cast<size_t>(k) * kLanes] : 0.0;
+          av[u] = k < end ? (sh ? __ldg(P.Ash + k) : P.A[ao + static_cast<size_t>(k) * kLanes]) : 0.0;
           pv[u] = k < end ? P.p[vo + static_cast<size_t>(cj) * kLanes] : 0.0;
         }
 #pragma unroll
@@ -340,7 +487,7 @@ __device__ __forceinline__ void spmv_long_rows(const PropParams& P, bool active,
     if (warp == 0 && active) {
       double qv = 0.0;
       for (int w = 0; w < kWarps; ++w) qv += lpart[w][lane];
-      spmv_epilogue<LINEAR>(P, i, vo, qv, acc);
+      spmv_epilogue(P, i, vo, qv, sh, acc);
     }
     __syncthreads();
   }
@@ -350,17 +497,17 @@ __device__ __forceinline__ void spmv_long_rows(const PropParams& P, bool active,
 // issued together): x += alpha p (x = alpha p on the first iteration),
 // r -= alpha q, z = D r, p = z + beta p; partials r.r and r.z.
 template <bool LINEAR>
-__device__ __forceinline__ void update_range(const PropParams& P, double* x, int rb, int re, size_t vo,
+__device__ __forceinline__ void update_range(const PropParams& P, double* x, int rb, int re, int stride, size_t vo,
                                              double alpha, double beta, bool first, double (&acc)[kNDots]) {
   constexpr int B = 4;
-  for (int i0 = rb; i0 < re; i0 += B) {
+  for (int i0 = rb; i0 < re; i0 += B * stride) {
     double dv[B], pv[B], qv[B], rv[B], xv[B];
 #pragma unroll
     for (int u = 0; u < B; ++u) {
-      const int i = i0 + u;
+      const int i = i0 + u * stride;
       const bool ok = i < re;
       const size_t iv = vo + static_cast<size_t>(ok ? i : i0) * kLanes;
-      dv[u] = ok ? (LINEAR ? __ldg(P.Dsh + i) : P.Dinv[iv]) : 0.0;
+      dv[u] = ok ? (row_shared(P, i) ? __ldg(P.Dsh + i) : P.Dinv[iv]) : 0.0;
       pv[u] = ok ? P.p[iv] : 0.0;
       qv[u] = ok ? P.q[iv] : 0.0;
       rv[u] = ok ? P.r[iv] : 0.0;
@@ -368,7 +515,7 @@ __device__ __forceinline__ void update_range(const PropParams& P, double* x, int
     }
 #pragma unroll
     for (int u = 0; u < B; ++u) {
-      const int i = i0 + u;
+      const int i = i0 + u * stride;
       if (i >= re) break;
       const size_t iv = vo + static_cast<size_t>(i) * kLanes;
       x[iv] = first ? alpha * pv[u] : xv[u] + alpha * pv[u];
@@ -409,8 +556,12 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   X.G = P.G;
   X.C = P.C;
   X.Lp = 32;
-  const int row_begin = P.warp_row_begin[c * kWarps + warp];
-  const int row_end = P.warp_row_begin[c * kWarps + warp + 1];
+  // rows of the block's range interleaved across its warps (row = begin + warp +
+  // 16 k): the warps sweep one contiguous window together, so the +-ntheta
+  // neighbour gathers of the SpMV hit L1 and the streamed arrays are read in
+  // contiguous 4 KB windows
+  const int row_begin = P.warp_row_begin[c * kWarps] + warp;
+  const int row_end = P.warp_row_begin[c * kWarps + kWarps];
   unsigned long long target = 0;
   int bar_idx = 0;
   const bool writer = (c == 0) && (warp == 0) && valid;
@@ -436,23 +587,29 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
 
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
   long long lockstep = 0;
+  // optional per-block timing (P.dbg): work / barrier-wait ns and counts for
+  // intervals where lane 0 ran phase A, phase B, or anything else
+  unsigned long long dbg[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 
   while (__syncthreads_or(act != ACT_IDLE)) {
+    unsigned long long t_start = 0, t_arr = 0;
+    if (P.dbg && threadIdx.x == 0) t_start = globaltimer_ns();
+    const int dbg_kind = act == ACT_A ? 0 : (act == ACT_B ? 1 : 2);
     const double t_now = (act != ACT_IDLE) ? P.t_next[static_cast<size_t>(step) * P.count + sys] : 0.0;
     double* xs = LINEAR ? ((step & 1) ? P.ubuf0 : P.ubuf1) : P.x;
     // ------------------------------------------------ this lane's action
     if (P.n_long > 0) spmv_long_rows<LINEAR>(P, act == ACT_A, vo, ao, c, lpart, acc);
     if (act == ACT_A) {
-      spmv_range<LINEAR>(P, row_begin, row_end, vo, ao, acc);
+      spmv_range<LINEAR>(P, row_begin, row_end, kWarps, vo, ao, acc);
     } else if (act == ACT_B) {
-      update_range<LINEAR>(P, xs, row_begin, row_end, vo, s.alpha, s.beta, s.pit == 0, acc);
+      update_range<LINEAR>(P, xs, row_begin, row_end, kWarps, vo, s.alpha, s.beta, s.pit == 0, acc);
     } else if (act == ACT_R0 || act == ACT_R) {
       if constexpr (!LINEAR)
-        for (int i = row_begin; i < row_end; ++i)
+        for (int i = row_begin; i < row_end; i += kWarps)
           refill_row<NPE>(P, sh_curves, i, sys, vo, ao, step, act == ACT_R0, acc);
     } else if (act == ACT_U) {
       if (!s.zero_dx)
-        for (int i = row_begin; i < row_end; ++i) {
+        for (int i = row_begin; i < row_end; i += kWarps) {
           // trial u += lambda delta (propagators.cpp:46-48), or a backtrack
           // u -= lambda delta with lambda already halved; delta must be finite
           const size_t iv = vo + static_cast<size_t>(i) * kLanes;
@@ -468,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       // b = M (u/dt) + f, x = 0, r = b, p = D b (proj/src/propagators.cpp:85-94)
       const double* uin = (step & 1) ? P.ubuf1 : P.ubuf0;
       const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
-      for (int i = row_begin; i < row_end; ++i) {
+      for (int i = row_begin; i < row_end; i += kWarps) {
         const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
         double mv = 0.0;
         for (int k = base; k < end; ++k)
@@ -486,14 +643,20 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       }
     } else if (act == ACT_LU) {
       // the step solution must be finite (propagators.cpp:92); x0 = 0 when b = 0
-      for (int i = row_begin; i < row_end; ++i) {
+      for (int i = row_begin; i < row_end; i += kWarps) {
         const size_t iv = vo + static_cast<size_t>(i) * kLanes;
         if (s.pit == 0) xs[iv] = 0.0;
         acc[0] += isfinite(xs[iv]) ? 0.0 : 1.0;
       }
     }
-    if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, target, bar_idx)) return;
+    if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, target, bar_idx, P.dbg ? &t_arr : nullptr)) return;
     ++lockstep;
+    if (P.dbg && threadIdx.x == 0) {
+      const unsigned long long t_end = globaltimer_ns();
+      dbg[3 * dbg_kind + 0] += t_arr - t_start;
+      dbg[3 * dbg_kind + 1] += t_end - t_arr;
+      dbg[3 * dbg_kind + 2] += 1;
+    }
     const double t0v = sh.tot[0][sl], t1v = sh.tot[1][sl], t2v = sh.tot[2][sl], t3v = sh.tot[3][sl];
     // ------------------------------------------------ this lane's transition
     switch (act) {
@@ -618,6 +781,42 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     P.out[sys] = o;
   }
   if (c == 0 && threadIdx.x == 0) P.lockstep[g] = lockstep;
+  if (P.dbg && threadIdx.x == 0)
+    for (int k = 0; k < 9; ++k) P.dbg[static_cast<size_t>(blockIdx.x) * 9 + k] = dbg[k];
+}
+
+// ------------------------------------------------------- phase probes
+// One PCG phase over the whole batch with the propagation kernel's exact thread
+// -> (group, row, lane) mapping and code, but no barriers or state machine:
+// a normal (non-cooperative) kernel that ncu can replay and that isolates the
+// memory behaviour of one phase.  mode 0: phase A (TMA-staged SpMV), 1: phase A
+// (register-pipelined SpMV), 2: phase B (update).  Dots go to `sink`.
+__global__ void __launch_bounds__(kThreads, 1) phase_probe_kernel(const PropParams P, int mode, double* sink) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x / P.C, c = blockIdx.x % P.C;
+  const size_t vo = static_cast<size_t>(g) * P.d * kLanes + lane;
+  const size_t ao = static_cast<size_t>(g) * P.nnz * kLanes + lane;
+  extern __shared__ __align__(128) unsigned char dsmem[];
+  StageBuf* bufs = reinterpret_cast<StageBuf*>(dsmem) + warp * kStages;
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(dsmem + sizeof(StageBuf) * kStages * kWarps) + warp * kStages;
+  unsigned cnt = 0, phases = 0;
+  if (mode == 0 && lane == 0) {
+    for (int s2 = 0; s2 < kStages; ++s2) mbar_init(bars + s2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  const int row_begin = P.warp_row_begin[c * kWarps] + warp;
+  const int row_end = P.warp_row_begin[c * kWarps + kWarps];
+  double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
+  if (mode == 0)
+    spmv_range_staged(P, row_begin, row_end, kWarps, vo, ao, true, bufs, bars, cnt, phases, acc);
+  else if (mode == 1)
+    spmv_range<false>(P, row_begin, row_end, kWarps, vo, ao, acc);
+  else
+    update_range<false>(P, P.x, row_begin, row_end, kWarps, vo, 1e-30, 1e-30, false, acc);
+  if (acc[0] == 12345.0) sink[blockIdx.x] = acc[1] + acc[2];  // keep the dots live
 }
 
 // ------------------------------------------------------------ small kernels
@@ -730,9 +929,15 @@ int max_coresident_blocks(bool linear, int npe, int* out) {
   // every variant must fit: the capacity is the minimum over all instantiations
   int best = 1 << 30;
   void* fns[] = {kernel_ptr<true, 0>(), kernel_ptr<false, 0>(), kernel_ptr<false, 2>(), kernel_ptr<false, 3>()};
-  for (void* fn : fns) {
+  for (int k = 0; k < 4; ++k) {
+    const size_t smem = 0;
+    if (smem &&
+        cudaFuncSetAttribute(fns[k], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+            cudaSuccess)
+      return PS_ERR_CUDA;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess) return PS_ERR_CUDA;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[k], kThreads, smem) != cudaSuccess)
+      return PS_ERR_CUDA;
     best = per_sm < best ? per_sm : best;
   }
   *out = sms * best;
@@ -743,7 +948,9 @@ int launch_propagate(const PropParams& prm, bool linear, int npe, cudaStream_t s
   void* fn = select_kernel(linear, npe);
   PropParams local = prm;
   void* args[] = {&local};
-  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(prm.G * prm.C), dim3(kThreads), args, 0, st);
+  const size_t smem = 0;
+  (void)linear;
+  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(prm.G * prm.C), dim3(kThreads), args, smem, st);
   if (e != cudaSuccess) {
     if (err) *err = std::string("cuda: propagate launch failed: ") + cudaGetErrorString(e);
     return PS_ERR_CUDA;
@@ -833,6 +1040,14 @@ void launch_axpby_shared(const double* a, double sa, const double* b, double sb,
 void launch_eval_curve(const ps_curve& c, int n, const double* b2, double* nu, double* nup, cudaStream_t st) {
   if (n <= 0) return;
   curve_kernel<<<(n + 255) / 256, 256, 0, st>>>(c, n, b2, nu, nup);
+}
+
+int launch_phase_probe(const PropParams& prm, int mode, double* sink, cudaStream_t st) {
+  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(phase_probe_kernel),
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStageSmem)) != cudaSuccess)
+    return PS_ERR_CUDA;
+  phase_probe_kernel<<<prm.G * prm.C, kThreads, kStageSmem, st>>>(prm, mode, sink);
+  return cudaGetLastError() == cudaSuccess ? PS_OK : PS_ERR_CUDA;
 }
 
 void launch_frozen_K(const DevProblem& p, const double* u_ref, double* K_out, cudaStream_t st) {

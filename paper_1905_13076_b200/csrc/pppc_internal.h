@@ -49,9 +49,12 @@ struct PropParams {
   const int* diag;
   const double* M;
   const double* Klin;     // linear K (Newton on a linear problem)
-  // shared (linear) step matrix and Jacobi diagonal
+  // shared step matrix M/dt + K (linear problems) or M/dt + K_const (element
+  // problems, rows of rowkind 0) and its Jacobi diagonal
   const double* Ash;
   const double* Dsh;
+  const unsigned char* rowkind;  // element problems: 1 = row touches a nonlinear element
+  const double* Kc;              // constant-nu stiffness (rows of rowkind 0)
   // element data (nonlinear)
   const int* adj_ptr;
   const int2* adj;        // (element, local index)
@@ -93,6 +96,7 @@ struct PropParams {
   SysOut* out;                // [count]
   double* trace;              // [count][newton_max] or null
   int64_t* lockstep;          // [G] lock-step PCG iterations executed
+  unsigned long long* dbg;    // optional [G*C][9] timing (PPPC_DEBUG_TIMING)
 };
 
 struct DftPlan;
@@ -124,6 +128,11 @@ struct DevProblem {
   std::vector<int> h_rp, h_ci, h_diag;
   std::vector<double> h_M, h_K;
   int max_row_len = 0;
+  // element problems: rows touching only constant-nu elements share their values
+  unsigned char* rowkind = nullptr;
+  double* Kc = nullptr;
+  std::vector<unsigned char> h_rowkind;
+  std::vector<double> h_Kc;
 };
 
 // launches (kernels.cu)
@@ -149,6 +158,7 @@ void launch_axpby_shared(const double* a, double sa, const double* b, double sb,
 void launch_eval_curve(const ps_curve& c, int n, const double* b2, double* nu, double* nup,
                        cudaStream_t st);
 void launch_frozen_K(const DevProblem& p, const double* u_ref, double* K_out, cudaStream_t st);
+int launch_phase_probe(const PropParams& prm, int mode, double* sink, cudaStream_t st);
 
 // spectral (spectral.cu)
 struct SpectralState;

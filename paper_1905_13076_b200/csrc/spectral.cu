@@ -522,7 +522,8 @@ struct SpectralState {
 };
 
 // shared with capi.cu
-int row_ranges(const std::vector<int>& h_rp, int C, int R, std::vector<int>* out);
+int row_ranges(const std::vector<int>& h_rp, int C, int R, std::vector<int>* out,
+               const std::vector<unsigned char>* rowkind);
 int long_rows_of(const std::vector<int>& h_rp, const std::vector<int>& ranges, std::vector<int>* rows,
                  std::vector<int>* owner);
 
@@ -618,7 +619,7 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
       return PS_ERR_BAD_ARG;
     }
     std::vector<int> ranges;
-    row_ranges(p.h_rp, s->C, s->R, &ranges);
+    row_ranges(p.h_rp, s->C, s->R, &ranges, nullptr);
     rc |= dalloc(&s->warp_row_begin, ranges.size());
     cudaMemcpy(s->warp_row_begin, ranges.data(), ranges.size() * sizeof(int), cudaMemcpyHostToDevice);
     std::vector<int> lrows, lowner;
