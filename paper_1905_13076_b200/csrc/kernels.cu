@@ -539,6 +539,12 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   __shared__ SyncShared<kNDots> sh;
   __shared__ ps_curve sh_curves[kMaxCurves];
   __shared__ double lpart[kWarps][32];
+  // Per-lane (= per-system) state lives once per block in shared memory: warp 0
+  // runs the transitions after each barrier, every warp reads what its action
+  // needs.  (Keeping a copy in every thread's registers would cost ~25 registers
+  // the SpMV pipeline needs.)
+  __shared__ Lane lanes[32];
+  __shared__ int lact[32], lstep[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x / P.C, c = blockIdx.x % P.C;
   const int sl = lane;
@@ -548,6 +554,26 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   const size_t ao = static_cast<size_t>(g) * P.nnz * kLanes + sl;
   if (threadIdx.x < P.ncurves) sh_curves[threadIdx.x] = P.curves[threadIdx.x];
   if (threadIdx.x == 0) sh.abort = 0;
+  if (warp == 0) {
+    Lane& s = lanes[lane];
+    s.alive = valid;
+    s.code = PS_OK;
+    s.t_fail = 0.0;
+    s.res_fail = 0.0;
+    s.tol = 0.0;
+    s.nit = 0;
+    s.pact = false;
+    s.pit = 0;
+    s.rho = s.stop = s.alpha = s.beta = 0.0;
+    s.res_pre = 0.0;
+    s.lambda = 1.0;
+    s.ls_k = 0;
+    s.bt = s.zero_dx = false;
+    s.newton_total = s.pcg_total = 0;
+    s.max_nit = s.max_pit = s.last_nit = 0;
+    lact[lane] = valid ? (LINEAR ? ACT_L0 : ACT_R0) : ACT_IDLE;
+    lstep[lane] = 0;
+  }
   __syncthreads();
   SyncCtx X;
   X.sync = P.sync;
@@ -557,70 +583,56 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   X.C = P.C;
   X.Lp = 32;
   // rows of the block's range interleaved across its warps (row = begin + warp +
-  // 16 k): the warps sweep one contiguous window together, so the +-ntheta
-  // neighbour gathers of the SpMV hit L1 and the streamed arrays are read in
-  // contiguous 4 KB windows
+  // 16 k): the warps sweep one contiguous window together and the streamed
+  // arrays are read in contiguous windows
   const int row_begin = P.warp_row_begin[c * kWarps] + warp;
   const int row_end = P.warp_row_begin[c * kWarps + kWarps];
   unsigned long long target = 0;
   int bar_idx = 0;
   const bool writer = (c == 0) && (warp == 0) && valid;
 
-  Lane s;
-  s.alive = valid;
-  s.code = PS_OK;
-  s.t_fail = 0.0;
-  s.res_fail = 0.0;
-  s.tol = 0.0;
-  s.nit = 0;
-  s.pact = false;
-  s.pit = 0;
-  s.rho = s.stop = s.alpha = s.beta = 0.0;
-  s.res_pre = 0.0;
-  s.lambda = 1.0;
-  s.ls_k = 0;
-  s.bt = s.zero_dx = false;
-  s.newton_total = s.pcg_total = 0;
-  s.max_nit = s.max_pit = s.last_nit = 0;
-  int act = valid ? (LINEAR ? ACT_L0 : ACT_R0) : ACT_IDLE;
-  int step = 0;
-
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
   long long lockstep = 0;
   // optional per-block timing (P.dbg): work / barrier-wait ns and counts for
   // intervals where lane 0 ran phase A, phase B, or anything else
-  unsigned long long dbg[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  __shared__ unsigned long long dbg[9];
+  if (threadIdx.x < 9) dbg[threadIdx.x] = 0;
 
-  while (__syncthreads_or(act != ACT_IDLE)) {
+  while (__syncthreads_or(lact[sl] != ACT_IDLE)) {
+    const int act = lact[sl];
+    const int step = lstep[sl];
     unsigned long long t_start = 0, t_arr = 0;
     if (P.dbg && threadIdx.x == 0) t_start = globaltimer_ns();
     const int dbg_kind = act == ACT_A ? 0 : (act == ACT_B ? 1 : 2);
-    const double t_now = (act != ACT_IDLE) ? P.t_next[static_cast<size_t>(step) * P.count + sys] : 0.0;
     double* xs = LINEAR ? ((step & 1) ? P.ubuf0 : P.ubuf1) : P.x;
     // ------------------------------------------------ this lane's action
     if (P.n_long > 0) spmv_long_rows<LINEAR>(P, act == ACT_A, vo, ao, c, lpart, acc);
     if (act == ACT_A) {
       spmv_range<LINEAR>(P, row_begin, row_end, kWarps, vo, ao, acc);
     } else if (act == ACT_B) {
-      update_range<LINEAR>(P, xs, row_begin, row_end, kWarps, vo, s.alpha, s.beta, s.pit == 0, acc);
+      update_range<LINEAR>(P, xs, row_begin, row_end, kWarps, vo, lanes[sl].alpha, lanes[sl].beta,
+                           lanes[sl].pit == 0, acc);
     } else if (act == ACT_R0 || act == ACT_R) {
       if constexpr (!LINEAR)
         for (int i = row_begin; i < row_end; i += kWarps)
           refill_row<NPE>(P, sh_curves, i, sys, vo, ao, step, act == ACT_R0, acc);
     } else if (act == ACT_U) {
-      if (!s.zero_dx)
+      if (!lanes[sl].zero_dx) {
+        const bool bt = lanes[sl].bt;
+        const double lambda = lanes[sl].lambda;
         for (int i = row_begin; i < row_end; i += kWarps) {
           // trial u += lambda delta (propagators.cpp:46-48), or a backtrack
           // u -= lambda delta with lambda already halved; delta must be finite
           const size_t iv = vo + static_cast<size_t>(i) * kLanes;
           const double dx = P.x[iv];
-          if (s.bt) {
-            P.u[iv] -= s.lambda * dx;
+          if (bt) {
+            P.u[iv] -= lambda * dx;
           } else {
             acc[0] += isfinite(dx) ? 0.0 : 1.0;
-            P.u[iv] += s.lambda * dx;
+            P.u[iv] += lambda * dx;
           }
         }
+      }
     } else if (act == ACT_L0) {
       // b = M (u/dt) + f, x = 0, r = b, p = D b (proj/src/propagators.cpp:85-94)
       const double* uin = (step & 1) ? P.ubuf1 : P.ubuf0;
@@ -643,9 +655,10 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       }
     } else if (act == ACT_LU) {
       // the step solution must be finite (propagators.cpp:92); x0 = 0 when b = 0
+      const bool zero = lanes[sl].pit == 0;
       for (int i = row_begin; i < row_end; i += kWarps) {
         const size_t iv = vo + static_cast<size_t>(i) * kLanes;
-        if (s.pit == 0) xs[iv] = 0.0;
+        if (zero) xs[iv] = 0.0;
         acc[0] += isfinite(xs[iv]) ? 0.0 : 1.0;
       }
     }
@@ -657,118 +670,128 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       dbg[3 * dbg_kind + 1] += t_end - t_arr;
       dbg[3 * dbg_kind + 2] += 1;
     }
-    const double t0v = sh.tot[0][sl], t1v = sh.tot[1][sl], t2v = sh.tot[2][sl], t3v = sh.tot[3][sl];
-    // ------------------------------------------------ this lane's transition
-    switch (act) {
-      case ACT_R0: {
-        s.tol = P.newton_tol_abs + P.newton_tol_rel * sqrt(t1v);
-        s.nit = 1;
-        s.res_pre = sqrt(t0v);
-        pcg_start(s, t2v, t3v, P.pcg_tol);
-        s.bt = false;
-        s.zero_dx = !s.pact;
-        s.lambda = P.damping;
-        s.ls_k = 0;
-        act = s.pact ? ACT_A : ACT_U;
-        break;
-      }
-      case ACT_A: {
-        if (!isfinite(t0v) || t0v == 0.0) {
-          lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
-        } else {
-          s.alpha = s.rho / t0v;
-          const double rho_est = s.rho - 2.0 * s.alpha * t1v + s.alpha * s.alpha * t2v;
-          s.beta = rho_est / s.rho;
-          act = ACT_B;
-        }
-        break;
-      }
-      case ACT_B: {
-        const double rr = t0v;
-        s.rho = t1v;
-        s.pit += 1;
-        if (rr <= s.stop) {
-          s.pact = false;
-          s.pcg_total += s.pit;
-          s.max_pit = max(s.max_pit, s.pit);
-          act = LINEAR ? ACT_LU : ACT_U;
-        } else if (!isfinite(rr)) {
-          lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
-        } else if (s.pit >= P.pcg_max) {
-          lane_fail(s, PS_ERR_PCG_MAXITER, LINEAR ? 0.0 : s.res_pre, t_now);
-        } else {
-          act = ACT_A;
-        }
-        break;
-      }
-      case ACT_U: {
-        if (!s.bt && t0v > 0.0)
-          lane_fail(s, PS_ERR_SINGULAR, s.res_pre, t_now);
-        else
-          act = ACT_R;
-        break;
-      }
-      case ACT_R: {
-        const double post = sqrt(t0v);
-        if (P.line_search > 0 && s.ls_k < P.line_search && !(post <= s.tol) &&
-            !(post <= (1.0 - 1e-4 * s.lambda) * s.res_pre)) {
-          s.lambda *= 0.5;
-          s.ls_k += 1;
-          s.bt = true;
-          act = ACT_U;
-          break;
-        }
-        s.bt = false;
-        if (writer && P.trace) P.trace[static_cast<size_t>(sys) * P.newton_max + (s.nit - 1)] = post;
-        if (!isfinite(post)) {
-          lane_fail(s, PS_ERR_NEWTON_DIVERGED, post, t_now);
-        } else if (post <= s.tol) {
-          s.newton_total += s.nit;
-          s.last_nit = s.nit;
-          s.max_nit = max(s.max_nit, s.nit);
-          ++step;
-          act = step < P.steps ? ACT_R0 : ACT_IDLE;
-        } else if (s.nit >= P.newton_max) {
-          lane_fail(s, PS_ERR_NEWTON_MAXITER, post, t_now);
-        } else {
-          s.nit += 1;
-          s.res_pre = post;
+    // ------------------------------------------------ transitions (warp 0)
+    if (warp == 0) {
+      Lane& s = lanes[lane];
+      int a = act;
+      int stp = step;
+      const double t_now = (a != ACT_IDLE) ? P.t_next[static_cast<size_t>(stp) * P.count + sys] : 0.0;
+      const double t0v = sh.tot[0][sl], t1v = sh.tot[1][sl], t2v = sh.tot[2][sl], t3v = sh.tot[3][sl];
+      switch (a) {
+        case ACT_R0: {
+          s.tol = P.newton_tol_abs + P.newton_tol_rel * sqrt(t1v);
+          s.nit = 1;
+          s.res_pre = sqrt(t0v);
           pcg_start(s, t2v, t3v, P.pcg_tol);
+          s.bt = false;
           s.zero_dx = !s.pact;
           s.lambda = P.damping;
           s.ls_k = 0;
-          act = s.pact ? ACT_A : ACT_U;
+          a = s.pact ? ACT_A : ACT_U;
+          break;
         }
-        break;
-      }
-      case ACT_L0: {
-        pcg_start(s, t0v, t1v, P.pcg_tol);
-        act = s.pact ? ACT_A : ACT_LU;
-        break;
-      }
-      case ACT_LU: {
-        if (t0v > 0.0) {
-          lane_fail(s, PS_ERR_SINGULAR, 0.0, t_now);
-        } else {
-          s.newton_total += 1;
-          s.last_nit = 1;
-          s.max_nit = max(s.max_nit, 1);
-          ++step;
-          act = step < P.steps ? ACT_L0 : ACT_IDLE;
+        case ACT_A: {
+          if (!isfinite(t0v) || t0v == 0.0) {
+            lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
+          } else {
+            s.alpha = s.rho / t0v;
+            const double rho_est = s.rho - 2.0 * s.alpha * t1v + s.alpha * s.alpha * t2v;
+            s.beta = rho_est / s.rho;
+            a = ACT_B;
+          }
+          break;
         }
-        break;
+        case ACT_B: {
+          const double rr = t0v;
+          s.rho = t1v;
+          s.pit += 1;
+          if (rr <= s.stop) {
+            s.pact = false;
+            s.pcg_total += s.pit;
+            s.max_pit = max(s.max_pit, s.pit);
+            a = LINEAR ? ACT_LU : ACT_U;
+          } else if (!isfinite(rr)) {
+            lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
+          } else if (s.pit >= P.pcg_max) {
+            lane_fail(s, PS_ERR_PCG_MAXITER, LINEAR ? 0.0 : s.res_pre, t_now);
+          } else {
+            a = ACT_A;
+          }
+          break;
+        }
+        case ACT_U: {
+          if (!s.bt && t0v > 0.0)
+            lane_fail(s, PS_ERR_SINGULAR, s.res_pre, t_now);
+          else
+            a = ACT_R;
+          break;
+        }
+        case ACT_R: {
+          const double post = sqrt(t0v);
+          if (P.line_search > 0 && s.ls_k < P.line_search && !(post <= s.tol) &&
+              !(post <= (1.0 - 1e-4 * s.lambda) * s.res_pre)) {
+            s.lambda *= 0.5;
+            s.ls_k += 1;
+            s.bt = true;
+            a = ACT_U;
+            break;
+          }
+          s.bt = false;
+          if (writer && P.trace) P.trace[static_cast<size_t>(sys) * P.newton_max + (s.nit - 1)] = post;
+          if (!isfinite(post)) {
+            lane_fail(s, PS_ERR_NEWTON_DIVERGED, post, t_now);
+          } else if (post <= s.tol) {
+            s.newton_total += s.nit;
+            s.last_nit = s.nit;
+            s.max_nit = max(s.max_nit, s.nit);
+            ++stp;
+            a = stp < P.steps ? ACT_R0 : ACT_IDLE;
+          } else if (s.nit >= P.newton_max) {
+            lane_fail(s, PS_ERR_NEWTON_MAXITER, post, t_now);
+          } else {
+            s.nit += 1;
+            s.res_pre = post;
+            pcg_start(s, t2v, t3v, P.pcg_tol);
+            s.zero_dx = !s.pact;
+            s.lambda = P.damping;
+            s.ls_k = 0;
+            a = s.pact ? ACT_A : ACT_U;
+          }
+          break;
+        }
+        case ACT_L0: {
+          pcg_start(s, t0v, t1v, P.pcg_tol);
+          a = s.pact ? ACT_A : ACT_LU;
+          break;
+        }
+        case ACT_LU: {
+          if (t0v > 0.0) {
+            lane_fail(s, PS_ERR_SINGULAR, 0.0, t_now);
+          } else {
+            s.newton_total += 1;
+            s.last_nit = 1;
+            s.max_nit = max(s.max_nit, 1);
+            ++stp;
+            a = stp < P.steps ? ACT_L0 : ACT_IDLE;
+          }
+          break;
+        }
+        case ACT_WAIT:
+          a = ACT_A;
+          break;
+        default:
+          break;
       }
-      case ACT_WAIT:
-        act = ACT_A;
-        break;
-      default:
-        break;
+      if (!s.alive) a = ACT_IDLE;
+      if (a == ACT_A && (lockstep & 1)) a = ACT_WAIT;  // phase A only on even intervals
+      lact[lane] = a;
+      lstep[lane] = stp;
     }
-    if (!s.alive) act = ACT_IDLE;
-    if (act == ACT_A && (lockstep & 1)) act = ACT_WAIT;  // phase A only on even intervals
+    __syncthreads();
   }
 
   if (writer) {
+    const Lane& s = lanes[lane];
     SysOut o;
     o.code = s.code;
     o.newton_last = s.last_nit;
