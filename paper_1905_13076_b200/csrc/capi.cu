@@ -521,6 +521,29 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   unsigned long long* dbg = nullptr;
   const int nblk = geo.G * geo.C;
   if (debug_timing && dalloc(&dbg, static_cast<size_t>(nblk) * 9)) K.dbg = dbg;
+  // The SpMV gathers the search direction p at +-ntheta rows; keep p resident in
+  // L2 (persisting access-policy window) so the streamed matrix values and
+  // vectors do not evict it between neighbour reads.  PPPC_NO_L2_PERSIST=1 off.
+  static const bool l2_persist = std::getenv("PPPC_NO_L2_PERSIST") == nullptr;
+  if (l2_persist) {
+    int dev = 0, max_persist = 0, max_window = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    const size_t pbytes = static_cast<size_t>(geo.G) * P.d * 32 * sizeof(double);
+    if (max_persist > 0 && max_window > 0) {
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(max_persist, pbytes));
+      cudaStreamAttrValue attr{};
+      attr.accessPolicyWindow.base_ptr = ctx->p;
+      attr.accessPolicyWindow.num_bytes = std::min<size_t>(pbytes, static_cast<size_t>(max_window));
+      attr.accessPolicyWindow.hitRatio =
+          std::min(1.0f, static_cast<float>(max_persist) / static_cast<float>(attr.accessPolicyWindow.num_bytes));
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+      cudaGetLastError();
+    }
+  }
   check(cudaEventRecord(ctx->e0, ctx->stream), "event");
   std::string err;
   const int rc = launch_propagate(K, linear_path, npe, ctx->stream, &err);
