@@ -34,6 +34,7 @@ struct Geometry {
   int n_long = 0;
   int* long_rows = nullptr;
   int* long_owner = nullptr;
+  int max_block_rows = 0;  // largest row range of one block (shared-memory records)
 };
 
 // Rows longer than kLongRow and the block whose warp ranges contain them.
@@ -116,7 +117,14 @@ struct ps_ctx {
   double* tnext = nullptr;
   size_t tnext_len = 0;
   std::map<int, Geometry> geo;
-  std::map<double, std::pair<double*, double*>> step_cache;  // dt -> (A, Dinv), linear_factor analogue
+  // dt -> shared step matrix M/dt + K (CSR values, Jacobi, per-row padded
+  // values for the SpMV row records); the linear_factor analogue
+  struct StepMatrix {
+    double* A = nullptr;
+    double* D = nullptr;
+    double* AE = nullptr;
+  };
+  std::map<double, StepMatrix> step_cache;
   SpectralState* spec = nullptr;
   int spec_N = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -307,6 +315,19 @@ void build_problem(ps_ctx* ctx, const ps_problem_desc* desc) {
     P.rowkind = upload(P.h_rowkind.data(), P.h_rowkind.size(), "row kinds");
     P.Kc = upload(P.h_Kc.data(), P.h_Kc.size(), "constant stiffness");
   }
+  {
+    // row records (pppc_internal.h kEll)
+    std::vector<int4> rec(static_cast<size_t>(P.d) * kRecInts4);
+    for (int i = 0; i < P.d; ++i) {
+      const int b = P.h_rp[i], len = P.h_rp[i + 1] - b;
+      int c[kEll];
+      for (int k = 0; k < kEll; ++k) c[k] = (k < len && len <= kEll) ? P.h_ci[b + k] : i;
+      rec[kRecInts4 * i] = make_int4(b, len, P.linear ? 0 : P.h_rowkind[i], 0);
+      rec[kRecInts4 * i + 1] = make_int4(c[0], c[1], c[2], c[3]);
+      rec[kRecInts4 * i + 2] = make_int4(c[4], c[5], c[6], c[7]);
+    }
+    P.rowrec = upload(rec.data(), rec.size(), "row records");
+  }
   P.nterms = desc->n_terms;
   P.period = desc->period;
   P.amp.assign(desc->amplitude, desc->amplitude + P.nterms);
@@ -358,6 +379,8 @@ Geometry& geometry(ps_ctx* ctx, int count) {
   std::vector<int> ranges;
   row_ranges(ctx->P.h_rp, g.C, g.R, &ranges, &ctx->P.h_rowkind);
   g.warp_row_begin = upload(ranges.data(), ranges.size(), "row ranges");
+  for (int c = 0; c < g.C; ++c)
+    g.max_block_rows = std::max(g.max_block_rows, ranges[(c + 1) * kWarps] - ranges[c * kWarps]);
   std::vector<int> lrows, lowner;
   long_rows_of(ctx->P.h_rp, ranges, &lrows, &lowner);
   g.n_long = static_cast<int>(lrows.size());
@@ -366,18 +389,26 @@ Geometry& geometry(ps_ctx* ctx, int count) {
   return ctx->geo.emplace(count, g).first->second;
 }
 
-std::pair<double*, double*> shared_step_matrix(ps_ctx* ctx, double dt) {
+ps_ctx::StepMatrix shared_step_matrix(ps_ctx* ctx, double dt) {
   auto it = ctx->step_cache.find(dt);
   if (it != ctx->step_cache.end()) return it->second;
   const DevProblem& P = ctx->P;
-  std::vector<double> A(P.nnz), D(P.d);
+  std::vector<double> A(P.nnz), D(P.d), AE(static_cast<size_t>(P.d) * kEll, 0.0);
   // linear problems: M/dt + K; element problems: M/dt + K_const (valid on rows
   // with rowkind 0, the only rows that read it)
   const std::vector<double>& Kref = P.linear ? P.h_K : P.h_Kc;
   for (int k = 0; k < P.nnz; ++k) A[k] = P.h_M[k] / dt + Kref[k];
-  for (int i = 0; i < P.d; ++i) D[i] = 1.0 / A[P.h_diag[i]];
-  auto pr = std::make_pair(upload(A.data(), A.size(), "step matrix"), upload(D.data(), D.size(), "jacobi"));
-  return ctx->step_cache.emplace(dt, pr).first->second;
+  for (int i = 0; i < P.d; ++i) {
+    D[i] = 1.0 / A[P.h_diag[i]];
+    const int b = P.h_rp[i], len = P.h_rp[i + 1] - b;
+    if (len <= kEll)
+      for (int k = 0; k < len; ++k) AE[static_cast<size_t>(i) * kEll + k] = A[b + k];
+  }
+  ps_ctx::StepMatrix m;
+  m.A = upload(A.data(), A.size(), "step matrix");
+  m.D = upload(D.data(), D.size(), "jacobi");
+  m.AE = upload(AE.data(), AE.size(), "step matrix rows");
+  return ctx->step_cache.emplace(dt, m).first->second;
 }
 
 void excitation_coef(const DevProblem& P, double t, double* out) {
@@ -462,14 +493,17 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.rp = P.rp;
   K.ci = P.ci;
   K.diag = P.diag;
+  K.rowrec = P.rowrec;
+  K.rec_rows = geo.max_block_rows * kRecInts4 * sizeof(int4) <= kRecSmemMax ? geo.max_block_rows : 0;
   K.M = P.M;
   K.Klin = P.K;
   K.Kc = P.Kc;
   {
     // shared step matrix M/dt + K (linear) or M/dt + K_const (constant-nu rows)
     const auto sm = shared_step_matrix(ctx, dt);
-    K.Ash = sm.first;
-    K.Dsh = sm.second;
+    K.Ash = sm.A;
+    K.Dsh = sm.D;
+    K.AshE = sm.AE;
   }
   // rows with per-system values: every row under newton_step on a linear problem
   // uses the shared matrix (J = K), element problems by rowkind
@@ -786,7 +820,7 @@ int ps_create(const ps_problem_desc* problem, const ps_time_mesh* mesh, const ps
 void ps_destroy(ps_ctx* ctx) {
   if (!ctx) return;
   DevProblem& P = ctx->P;
-  void* ptrs[] = {P.rowkind, P.Kc, P.rp, P.ci, P.diag, P.M, P.K, P.adj_ptr, P.adj, P.adj_rel, P.en, P.eS, P.einvA, P.ecurve,
+  void* ptrs[] = {P.rowrec, P.rowkind, P.Kc, P.rp, P.ci, P.diag, P.M, P.K, P.adj_ptr, P.adj, P.adj_rel, P.en, P.eS, P.einvA, P.ecurve,
                   P.pat, ctx->u, ctx->uprev, ctx->x, ctx->r, ctx->p, ctx->q, ctx->Dinv, ctx->A, ctx->io_a,
                   ctx->io_b, ctx->sync, ctx->partials, ctx->abort_flag, ctx->out, ctx->trace, ctx->lockstep,
                   ctx->coef, ctx->tnext};
@@ -798,8 +832,9 @@ void ps_destroy(ps_ctx* ctx) {
     cudaFree(kv.second.long_owner);
   }
   for (auto& kv : ctx->step_cache) {
-    cudaFree(kv.second.first);
-    cudaFree(kv.second.second);
+    cudaFree(kv.second.A);
+    cudaFree(kv.second.D);
+    cudaFree(kv.second.AE);
   }
   if (ctx->spec) spectral_free(ctx->spec);
   if (ctx->e0) cudaEventDestroy(ctx->e0);

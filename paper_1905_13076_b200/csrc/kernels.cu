@@ -21,6 +21,7 @@
 #include "group_sync.cuh"
 #include "pppc_internal.h"
 
+#include <algorithm>
 #include <cstdio>
 
 namespace pppc {
@@ -365,92 +366,113 @@ __device__ __forceinline__ void spmv_range_staged(const PropParams& P, int rb, i
   }
 }
 
-// Phase A over a warp's row range: q = A p with the next row's column indices
-// and matrix values prefetched while the current row's gathered operands are
-// in flight (one dependent load round per row instead of two).  Long rows are
-// skipped (spmv_long_rows); rows between kRegularRow and kLongRow slots take a
-// plain loop.
+// Phase A, one row: every load of row i is issued from its record (pppc_internal.h
+// kEll; staged in shared memory by the persistent kernels) in one go, one row
+// ahead of its use: the padded column list drives eight unpredicated gathers
+// of p (pad columns point at the row itself and carry a = 0), the values come
+// from the padded shared rows (AshE: four uniform 16-byte loads, zero pads) or
+// the lane's per-system copy (one coalesced 256-byte segment per slot,
+// immediate offsets off one row pointer; slots past the row length read
+// nothing and hold 0), plus the row's own p, r and Jacobi entries.
+struct RowData {
+  int base, len;
+  bool shared;
+  double a[kEll], pv[kEll];
+  double po, ro, dv;
+};
+
+__device__ __forceinline__ void issue_row(const PropParams& P, const int4* rec, int i, const double* pb,
+                                          const double* rb, const double* db, const double* Ab, RowData& o) {
+  const int4 h = rec[kRecInts4 * i];
+  const int4 c03 = rec[kRecInts4 * i + 1], c47 = rec[kRecInts4 * i + 2];
+  o.base = h.x;
+  o.len = h.y;
+  o.shared = P.rowkind == nullptr || h.z == 0;
+  const int c[kEll] = {c03.x, c03.y, c03.z, c03.w, c47.x, c47.y, c47.z, c47.w};
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) o.pv[k] = pb[static_cast<ptrdiff_t>(c[k]) * kLanes];
+  const size_t io = static_cast<size_t>(i) * kLanes;
+  o.po = pb[io];
+  o.ro = rb[io];
+  if (o.shared) {
+    o.dv = __ldg(P.Dsh + i);
+    const double2* ap = reinterpret_cast<const double2*>(P.AshE + static_cast<size_t>(i) * kEll);
+#pragma unroll
+    for (int k = 0; k < kEll / 2; ++k) {
+      const double2 v = __ldg(ap + k);
+      o.a[2 * k] = v.x;
+      o.a[2 * k + 1] = v.y;
+    }
+  } else {
+    o.dv = db[io];
+    const int n = o.len <= kEll ? o.len : 0;
+    const double* ap = Ab + static_cast<size_t>(o.base) * kLanes;
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) o.a[k] = k < n ? ap[k * kLanes] : 0.0;
+  }
+}
+
+// Row i of phase A from `cur` (issued one row earlier); issues row i1 into `nxt`.
 template <bool LINEAR>
-__device__ __forceinline__ void spmv_range(const PropParams& P, int rb, int re, int stride, size_t vo, size_t ao,
-                                           double (&acc)[kNDots]) {
+__device__ __forceinline__ void spmv_row(const PropParams& P, const int4* rec, int i, int i1, bool more,
+                                         const double* pb, const double* rbp, const double* dbp, const double* Ab,
+                                         double* qb, const RowData& cur, RowData& nxt, double (&acc)[kNDots]) {
+  if (more) issue_row(P, rec, i1, pb, rbp, dbp, Ab, nxt);
+  double qv = 0.0;
+  if (cur.len <= kEll) {
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) qv += cur.a[k] * cur.pv[k];
+  } else if (cur.len <= kLongRow) {
+    for (int k = cur.base; k < cur.base + cur.len; ++k) {
+      const double av = cur.shared ? __ldg(P.Ash + k) : Ab[static_cast<size_t>(k) * kLanes];
+      qv += av * pb[static_cast<ptrdiff_t>(__ldg(P.ci + k)) * kLanes];
+    }
+  } else {
+    return;  // long rows: spmv_long_rows
+  }
+  qb[static_cast<size_t>(i) * kLanes] = qv;
+  const double zi = cur.dv * cur.ro;
+  acc[0] += cur.po * qv;
+  acc[1] += qv * zi;
+  acc[2] += qv * (cur.dv * qv);
+}
+
+// Phase A over a warp's rows (rb, rb + stride, ... < re): q = A p and the
+// partials p.q, q.z, q.Dq.  Unrolled by two so the in-flight and the consumed
+// operand sets keep fixed registers.
+template <bool LINEAR>
+__device__ __forceinline__ void spmv_range(const PropParams& P, const int4* rec, int rb, int re, int stride,
+                                           size_t vo, size_t ao, double (&acc)[kNDots]) {
   if (rb >= re) return;
-  (void)sizeof(LINEAR);
-  int c0[kRegularRow];
-  double a0[kRegularRow];
-  int i = rb;
-  int b0 = __ldg(P.rp + i), l0 = __ldg(P.rp + i + 1) - b0;
-  bool s0 = row_shared(P, i);
-  // own-row operands of the epilogue (p_i, r_i, Dinv_i), prefetched with the row
-  double po0, ro0, do0;
-  {
-    const size_t iv = vo + static_cast<size_t>(i) * kLanes;
-    po0 = P.p[iv];
-    ro0 = P.r[iv];
-    do0 = s0 ? __ldg(P.Dsh + i) : P.Dinv[iv];
-  }
-#pragma unroll
-  for (int k = 0; k < kRegularRow; ++k) {
-    c0[k] = k < l0 ? __ldg(P.ci + b0 + k) : i;
-    a0[k] = k < l0 ? (s0 ? __ldg(P.Ash + b0 + k) : P.A[ao + static_cast<size_t>(b0 + k) * kLanes]) : 0.0;
-  }
-  while (i < re) {
-    double pv[kRegularRow];
-    const bool reg = l0 <= kRegularRow;
-#pragma unroll
-    for (int k = 0; k < kRegularRow; ++k)
-      pv[k] = (reg && k < l0) ? P.p[vo + static_cast<size_t>(c0[k]) * kLanes] : 0.0;
-    // prefetch the next row's indices, values and own-row operands
-    const int i1 = i + stride;
-    int b1 = 0, l1 = 0;
-    bool s1 = true;
-    int c1[kRegularRow];
-    double a1[kRegularRow];
-    double po1 = 0.0, ro1 = 0.0, do1 = 0.0;
-    if (i1 < re) {
-      b1 = __ldg(P.rp + i1);
-      l1 = __ldg(P.rp + i1 + 1) - b1;
-      s1 = row_shared(P, i1);
-      const size_t iv1 = vo + static_cast<size_t>(i1) * kLanes;
-      po1 = P.p[iv1];
-      ro1 = P.r[iv1];
-      do1 = s1 ? __ldg(P.Dsh + i1) : P.Dinv[iv1];
-    }
-#pragma unroll
-    for (int k = 0; k < kRegularRow; ++k) {
-      c1[k] = k < l1 ? __ldg(P.ci + b1 + k) : i1;
-      a1[k] = k < l1 ? (s1 ? __ldg(P.Ash + b1 + k) : P.A[ao + static_cast<size_t>(b1 + k) * kLanes]) : 0.0;
-    }
-    if (reg) {
-      double qv = 0.0;
-#pragma unroll
-      for (int k = 0; k < kRegularRow; ++k)
-        if (k < l0) qv += a0[k] * pv[k];
-      P.q[vo + static_cast<size_t>(i) * kLanes] = qv;
-      const double zi = do0 * ro0;
-      acc[0] += po0 * qv;
-      acc[1] += qv * zi;
-      acc[2] += qv * (do0 * qv);
-    } else if (l0 <= kLongRow) {
-      double qv = 0.0;
-      for (int k = b0; k < b0 + l0; ++k) {
-        const double av = s0 ? __ldg(P.Ash + k) : P.A[ao + static_cast<size_t>(k) * kLanes];
-        qv += av * P.p[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes];
-      }
-      spmv_epilogue(P, i, vo, qv, s0, acc);
-    }
+  const double* pb = P.p + vo;
+  const double* rbp = P.r + vo;
+  const double* dbp = P.Dinv + vo;
+  const double* Ab = P.A + ao;
+  double* qb = P.q + vo;
+  RowData ra, rc;
+  issue_row(P, rec, rb, pb, rbp, dbp, Ab, ra);
+  for (int i = rb;;) {
+    int i1 = i + stride;
+    spmv_row<LINEAR>(P, rec, i, i1, i1 < re, pb, rbp, dbp, Ab, qb, ra, rc, acc);
+    if (i1 >= re) break;
     i = i1;
-    b0 = b1;
-    l0 = l1;
-    s0 = s1;
-    po0 = po1;
-    ro0 = ro1;
-    do0 = do1;
-#pragma unroll
-    for (int k = 0; k < kRegularRow; ++k) {
-      c0[k] = c1[k];
-      a0[k] = a1[k];
-    }
+    i1 = i + stride;
+    spmv_row<LINEAR>(P, rec, i, i1, i1 < re, pb, rbp, dbp, Ab, qb, rc, ra, acc);
+    if (i1 >= re) break;
+    i = i1;
   }
+}
+
+// The block's row records in shared memory (P.rec_rows > 0), else the global
+// copy; the returned pointer is indexed by global row.
+__device__ __forceinline__ const int4* stage_records(const PropParams& P, int c, int4* srec) {
+  if (P.rec_rows <= 0) return P.rowrec;
+  const int r0 = P.warp_row_begin[c * kWarps], r1 = P.warp_row_begin[c * kWarps + kWarps];
+  const int n = (r1 - r0) * kRecInts4;
+  const int4* src = P.rowrec + static_cast<size_t>(r0) * kRecInts4;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) srec[t] = __ldg(src + t);
+  __syncthreads();
+  return srec - static_cast<ptrdiff_t>(r0) * kRecInts4;
 }
 
 // Long rows (the polar hub: ntheta+1 slots) walked serially by one lane would
@@ -497,8 +519,9 @@ __device__ __forceinline__ void spmv_long_rows(const PropParams& P, bool active,
 // issued together): x += alpha p (x = alpha p on the first iteration),
 // r -= alpha q, z = D r, p = z + beta p; partials r.r and r.z.
 template <bool LINEAR>
-__device__ __forceinline__ void update_range(const PropParams& P, double* x, int rb, int re, int stride, size_t vo,
-                                             double alpha, double beta, bool first, double (&acc)[kNDots]) {
+__device__ __forceinline__ void update_range(const PropParams& P, const int4* rec, double* x, int rb, int re,
+                                             int stride, size_t vo, double alpha, double beta, bool first,
+                                             double (&acc)[kNDots]) {
   constexpr int B = 4;
   for (int i0 = rb; i0 < re; i0 += B * stride) {
     double dv[B], pv[B], qv[B], rv[B], xv[B];
@@ -506,8 +529,10 @@ __device__ __forceinline__ void update_range(const PropParams& P, double* x, int
     for (int u = 0; u < B; ++u) {
       const int i = i0 + u * stride;
       const bool ok = i < re;
-      const size_t iv = vo + static_cast<size_t>(ok ? i : i0) * kLanes;
-      dv[u] = ok ? (row_shared(P, i) ? __ldg(P.Dsh + i) : P.Dinv[iv]) : 0.0;
+      const int ii = ok ? i : i0;
+      const size_t iv = vo + static_cast<size_t>(ii) * kLanes;
+      const bool sh = P.rowkind == nullptr || rec[kRecInts4 * ii].z == 0;
+      dv[u] = ok ? (sh ? __ldg(P.Dsh + ii) : P.Dinv[iv]) : 0.0;
       pv[u] = ok ? P.p[iv] : 0.0;
       qv[u] = ok ? P.q[iv] : 0.0;
       rv[u] = ok ? P.r[iv] : 0.0;
@@ -575,6 +600,8 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     lstep[lane] = 0;
   }
   __syncthreads();
+  extern __shared__ __align__(16) int4 srec[];
+  const int4* rec = stage_records(P, c, srec);
   SyncCtx X;
   X.sync = P.sync;
   X.partials = P.partials;
@@ -608,9 +635,9 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     // ------------------------------------------------ this lane's action
     if (P.n_long > 0) spmv_long_rows<LINEAR>(P, act == ACT_A, vo, ao, c, lpart, acc);
     if (act == ACT_A) {
-      spmv_range<LINEAR>(P, row_begin, row_end, kWarps, vo, ao, acc);
+      spmv_range<LINEAR>(P, rec, row_begin, row_end, kWarps, vo, ao, acc);
     } else if (act == ACT_B) {
-      update_range<LINEAR>(P, xs, row_begin, row_end, kWarps, vo, lanes[sl].alpha, lanes[sl].beta,
+      update_range<LINEAR>(P, rec, xs, row_begin, row_end, kWarps, vo, lanes[sl].alpha, lanes[sl].beta,
                            lanes[sl].pit == 0, acc);
     } else if (act == ACT_R0 || act == ACT_R) {
       if constexpr (!LINEAR)
@@ -832,13 +859,14 @@ __global__ void __launch_bounds__(kThreads, 1) phase_probe_kernel(const PropPara
   __syncthreads();
   const int row_begin = P.warp_row_begin[c * kWarps] + warp;
   const int row_end = P.warp_row_begin[c * kWarps + kWarps];
+  const int4* rec = mode == 0 ? P.rowrec : stage_records(P, c, reinterpret_cast<int4*>(dsmem));
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
   if (mode == 0)
     spmv_range_staged(P, row_begin, row_end, kWarps, vo, ao, true, bufs, bars, cnt, phases, acc);
   else if (mode == 1)
-    spmv_range<false>(P, row_begin, row_end, kWarps, vo, ao, acc);
+    spmv_range<false>(P, rec, row_begin, row_end, kWarps, vo, ao, acc);
   else
-    update_range<false>(P, P.x, row_begin, row_end, kWarps, vo, 1e-30, 1e-30, false, acc);
+    update_range<false>(P, rec, P.x, row_begin, row_end, kWarps, vo, 1e-30, 1e-30, false, acc);
   if (acc[0] == 12345.0) sink[blockIdx.x] = acc[1] + acc[2];  // keep the dots live
 }
 
@@ -953,7 +981,7 @@ int max_coresident_blocks(bool linear, int npe, int* out) {
   int best = 1 << 30;
   void* fns[] = {kernel_ptr<true, 0>(), kernel_ptr<false, 0>(), kernel_ptr<false, 2>(), kernel_ptr<false, 3>()};
   for (int k = 0; k < 4; ++k) {
-    const size_t smem = 0;
+    const size_t smem = kRecSmemMax;
     if (smem &&
         cudaFuncSetAttribute(fns[k], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
             cudaSuccess)
@@ -971,8 +999,7 @@ int launch_propagate(const PropParams& prm, bool linear, int npe, cudaStream_t s
   void* fn = select_kernel(linear, npe);
   PropParams local = prm;
   void* args[] = {&local};
-  const size_t smem = 0;
-  (void)linear;
+  const size_t smem = static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4);
   const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(prm.G * prm.C), dim3(kThreads), args, smem, st);
   if (e != cudaSuccess) {
     if (err) *err = std::string("cuda: propagate launch failed: ") + cudaGetErrorString(e);
@@ -1066,10 +1093,11 @@ void launch_eval_curve(const ps_curve& c, int n, const double* b2, double* nu, d
 }
 
 int launch_phase_probe(const PropParams& prm, int mode, double* sink, cudaStream_t st) {
+  const size_t smem = std::max(kStageSmem, static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4));
   if (cudaFuncSetAttribute(reinterpret_cast<const void*>(phase_probe_kernel),
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStageSmem)) != cudaSuccess)
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
     return PS_ERR_CUDA;
-  phase_probe_kernel<<<prm.G * prm.C, kThreads, kStageSmem, st>>>(prm, mode, sink);
+  phase_probe_kernel<<<prm.G * prm.C, kThreads, smem, st>>>(prm, mode, sink);
   return cudaGetLastError() == cudaSuccess ? PS_OK : PS_ERR_CUDA;
 }
 

@@ -19,6 +19,13 @@ constexpr int kMaxTerms = 16;
 constexpr int kNDots = 4;
 constexpr int kRegularRow = 7;         // rows with <= 7 slots (the P1 polar mesh) use register accumulators
 constexpr int kLongRow = 32;           // rows with > 32 slots are split across a block's warps
+// Row records: rowrec[3i] = {first slot, length, kind (1 = per-system values),
+// 0}; rowrec[3i+1..3i+2] = the row's column indices padded to kEll with the
+// row's own index (rows longer than kEll keep using row_ptr / col_idx).  The
+// persistent kernels copy their block's records into shared memory once.
+constexpr int kEll = 8;
+constexpr int kRecInts4 = 3;                          // int4 per row record
+constexpr size_t kRecSmemMax = 176 * 1024;            // dynamic shared memory for records
 
 // Per-system outcome written by block 0 of every group.
 struct SysOut {
@@ -47,12 +54,15 @@ struct PropParams {
   const int* rp;
   const int* ci;
   const int* diag;
+  const int4* rowrec;   // [d][kRecInts4]
+  int rec_rows;          // >0: largest block row range; records are staged in shared memory
   const double* M;
   const double* Klin;     // linear K (Newton on a linear problem)
   // shared step matrix M/dt + K (linear problems) or M/dt + K_const (element
   // problems, rows of rowkind 0) and its Jacobi diagonal
   const double* Ash;
   const double* Dsh;
+  const double* AshE;  // [d][kEll] padded rows of Ash (rows of <= kEll slots)
   const unsigned char* rowkind;  // element problems: 1 = row touches a nonlinear element
   const double* Kc;              // constant-nu stiffness (rows of rowkind 0)
   // element data (nonlinear)
@@ -110,6 +120,7 @@ struct DevProblem {
   int* rp = nullptr;
   int* ci = nullptr;
   int* diag = nullptr;
+  int4* rowrec = nullptr;
   double* M = nullptr;
   double* K = nullptr;        // linear K (or frozen K-bar)
   int* adj_ptr = nullptr;
