@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpppc_b200.so")
+# PPPC_LIB: load another build of the library (kernel-variant experiments)
+LIB_PATH = os.environ.get("PPPC_LIB") or os.path.join(_HERE, "libpppc_b200.so")
 
 PS_OK = 0
 PS_ERR_BAD_ARG = 1

@@ -360,6 +360,12 @@ void ensure(double** buf, size_t* len, size_t need) {
   *len = need;
 }
 
+// Chunk-to-block rotation (kernels.cu warp_rows); PPPC_CHUNK_ROT, diagnostics only.
+int chunk_rotation() {
+  static const int rot = std::getenv("PPPC_CHUNK_ROT") ? std::atoi(std::getenv("PPPC_CHUNK_ROT")) : 0;
+  return rot < 0 ? 0 : rot;
+}
+
 Geometry& geometry(ps_ctx* ctx, int count) {
   auto it = ctx->geo.find(count);
   if (it != ctx->geo.end()) return it->second;
@@ -379,10 +385,16 @@ Geometry& geometry(ps_ctx* ctx, int count) {
   std::vector<int> ranges;
   row_ranges(ctx->P.h_rp, g.C, g.R, &ranges, &ctx->P.h_rowkind);
   g.warp_row_begin = upload(ranges.data(), ranges.size(), "row ranges");
-  for (int c = 0; c < g.C; ++c)
-    g.max_block_rows = std::max(g.max_block_rows, ranges[(c + 1) * kWarps] - ranges[c * kWarps]);
+  // rows in chunks of kWarps dealt round-robin to the C blocks (kernels.cu
+  // warp_rows); a block holds at most ceil(chunks / C) chunks
+  const int chunks = (ctx->P.d + kWarps - 1) / kWarps;
+  g.max_block_rows = ((chunks + g.C - 1) / g.C) * kWarps;
   std::vector<int> lrows, lowner;
-  long_rows_of(ctx->P.h_rp, ranges, &lrows, &lowner);
+  for (int i = 0; i < ctx->P.d; ++i)
+    if (ctx->P.h_rp[i + 1] - ctx->P.h_rp[i] > kLongRow) {
+      lrows.push_back(i);
+      lowner.push_back((i / kWarps + chunk_rotation()) % g.C);
+    }
   g.n_long = static_cast<int>(lrows.size());
   g.long_rows = upload(lrows.data(), lrows.size(), "long rows");
   g.long_owner = upload(lowner.data(), lowner.size(), "long rows");
@@ -494,6 +506,13 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.ci = P.ci;
   K.diag = P.diag;
   K.rowrec = P.rowrec;
+  K.chunk_rot = chunk_rotation();
+  {
+    // phase-A L2 prefetch distance in rows, PPPC_PF (default 0 = off: it helps
+    // the standalone phase probe but not the persistent kernel)
+    static const int pf = std::getenv("PPPC_PF") ? std::atoi(std::getenv("PPPC_PF")) : 0;
+    K.pf_dist = pf < 0 ? 0 : pf;
+  }
   K.rec_rows = geo.max_block_rows * kRecInts4 * sizeof(int4) <= kRecSmemMax ? geo.max_block_rows : 0;
   K.M = P.M;
   K.Klin = P.K;
@@ -554,7 +573,7 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   static const bool debug_timing = std::getenv("PPPC_DEBUG_TIMING") != nullptr;
   unsigned long long* dbg = nullptr;
   const int nblk = geo.G * geo.C;
-  if (debug_timing && dalloc(&dbg, static_cast<size_t>(nblk) * 9)) K.dbg = dbg;
+  if (debug_timing && dalloc(&dbg, static_cast<size_t>(nblk) * kDbgSlots)) K.dbg = dbg;
   // The SpMV gathers the search direction p at +-ntheta rows; keep p resident in
   // L2 (persisting access-policy window) so the streamed matrix values and
   // vectors do not evict it between neighbour reads.  PPPC_NO_L2_PERSIST=1 off.
@@ -583,8 +602,11 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   const int rc = launch_propagate(K, linear_path, npe, ctx->stream, &err);
   if (rc != PS_OK) throw Failure(rc, err);
   check(cudaEventRecord(ctx->e1, ctx->stream), "event");
+  std::vector<unsigned long long> h_dbg;
   if (K.dbg) {
-    std::vector<unsigned long long> h(static_cast<size_t>(nblk) * 9);
+    constexpr int W = kDbgSlots;
+    std::vector<unsigned long long>& h = h_dbg;
+    h.resize(static_cast<size_t>(nblk) * W);
     check(cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream), "dbg");
     check(cudaStreamSynchronize(ctx->stream), "dbg");
     cudaFree(dbg);
@@ -592,11 +614,11 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
     for (int kind = 0; kind < 3; ++kind) {
       double work = 0, wait = 0, wmin = 1e300, wmax = 0, n = 0;
       for (int b = 0; b < nblk; ++b) {
-        const double cnt = static_cast<double>(h[b * 9 + 3 * kind + 2]);
+        const double cnt = static_cast<double>(h[b * W + 3 * kind + 2]);
         if (cnt == 0) continue;
-        const double w = h[b * 9 + 3 * kind] / cnt;
-        work += h[b * 9 + 3 * kind];
-        wait += h[b * 9 + 3 * kind + 1];
+        const double w = h[b * W + 3 * kind] / cnt;
+        work += h[b * W + 3 * kind];
+        wait += h[b * W + 3 * kind + 1];
         n += cnt;
         wmin = std::min(wmin, w);
         wmax = std::max(wmax, w);
@@ -608,11 +630,24 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
       if (kind < 2 && std::getenv("PPPC_DEBUG_BLOCKS")) {
         std::fprintf(stderr, "[pppc blocks %s]", names[kind]);
         for (int b = 0; b < nblk; ++b) {
-          const double cnt = static_cast<double>(h[b * 9 + 3 * kind + 2]);
-          std::fprintf(stderr, " %.0f", cnt > 0 ? h[b * 9 + 3 * kind] / cnt / 1e3 : 0.0);
+          const double cnt = static_cast<double>(h[b * W + 3 * kind + 2]);
+          std::fprintf(stderr, " %.0f", cnt > 0 ? h[b * W + 3 * kind] / cnt / 1e3 : 0.0);
         }
         std::fprintf(stderr, "\n");
       }
+    }
+  }
+  if (K.dbg) {
+    // lane-interval shares per action, block 0 of every group
+    const char* an[9] = {"idle", "R0", "A", "B", "U", "R", "L0", "LU", "wait"};
+    for (int gg = 0; gg < geo.G; ++gg) {
+      const unsigned long long* hb = h_dbg.data() + static_cast<size_t>(gg) * geo.C * kDbgSlots;
+      double tot = 0;
+      for (int a = 0; a < 9; ++a) tot += static_cast<double>(hb[9 + a]);
+      std::fprintf(stderr, "[pppc actions g%d] lane-intervals %.0f:", gg, tot);
+      for (int a = 0; a < 9; ++a)
+        if (hb[9 + a]) std::fprintf(stderr, " %s %.3f", an[a], hb[9 + a] / tot);
+      std::fprintf(stderr, "\n");
     }
   }
   std::vector<SysOut> outs(count);
@@ -626,6 +661,17 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   float ms = 0.0f;
   cudaEventElapsedTime(&ms, ctx->e0, ctx->e1);
   if (abort_h) throw Failure(PS_ERR_WATCHDOG, "cuda: device barrier watchdog fired in the propagation kernel");
+  if (K.dbg)
+    for (int gg = 0; gg < geo.G; ++gg) {
+      int64_t pmax = 0, psum = 0;
+      int nl = 0;
+      for (int l = 0; l < geo.L && gg * geo.L + l < count; ++l, ++nl) {
+        pmax = std::max<int64_t>(pmax, outs[gg * geo.L + l].pcg_total);
+        psum += outs[gg * geo.L + l].pcg_total;
+      }
+      std::fprintf(stderr, "[pppc group g%d] intervals %lld, lanes %d, pcg per lane max %lld mean %.0f\n", gg,
+                   static_cast<long long>(lock[gg]), nl, static_cast<long long>(pmax), nl ? double(psum) / nl : 0.0);
+    }
 
   ps_batch_status st{};
   st.failed_index = -1;
@@ -1339,7 +1385,7 @@ int ps_phase_probe(ps_ctx* ctx, int32_t mode, int32_t reps, double* ms_out, doub
     cudaFree(sink);
     const double d = K.d, nnz = K.nnz, nb = K.count;
     if (ms_out) *ms_out = ms / reps;
-    if (bytes_out) *bytes_out = mode == 2 ? nb * 64.0 * d : nb * (8.0 * nnz + 40.0 * d);
+    if (bytes_out) *bytes_out = mode >= 2 ? nb * 64.0 * d : nb * (8.0 * nnz + 40.0 * d);
   });
 }
 

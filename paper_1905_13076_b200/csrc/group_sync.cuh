@@ -36,7 +36,19 @@ struct SyncShared {
   double red[S][NDMAX][32];
   double tot[NDMAX][32];
   int abort;
+  // barrier state (thread 0 advances it): arrival target and barrier count
+  unsigned long long target;
+  int bar_idx;
 };
+
+template <int NDMAX>
+__device__ __forceinline__ void sync_state_init(SyncShared<NDMAX>& sh) {
+  if (threadIdx.x == 0) {
+    sh.abort = 0;
+    sh.target = 0;
+    sh.bar_idx = 0;
+  }
+}
 
 struct SyncCtx {
   unsigned long long* sync;  // [G]
@@ -46,9 +58,11 @@ struct SyncCtx {
 };
 
 // acc: this thread's partial sums (lane = system, sub-rows combined here).
+// The barrier state lives in `sh` (sync_state_init before the first call), so
+// nothing of it occupies registers across the caller's work loop.
 template <int NDMAX, int ND>
 __device__ bool group_sync_reduce(const SyncCtx& X, SyncShared<NDMAX>& sh, double (&acc)[NDMAX], int g, int c,
-                                  unsigned long long& target, int& bar_idx, unsigned long long* t_arrive = nullptr) {
+                                  unsigned long long* t_arrive = nullptr) {
   static_assert(ND <= NDMAX, "too many dots");
   constexpr int S = SyncShared<NDMAX>::S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -60,8 +74,8 @@ __device__ bool group_sync_reduce(const SyncCtx& X, SyncShared<NDMAX>& sh, doubl
 #pragma unroll
     for (int k = 0; k < ND; ++k) sh.wpart[warp][k][lane] = acc[k];
   }
+  const int buf = sh.bar_idx & 1;
   __syncthreads();
-  const int buf = bar_idx & 1;
   double* part = X.partials + ((static_cast<size_t>(buf) * X.G + g) * X.C) * (NDMAX * 32);
   if (threadIdx.x < ND * 32) {
     const int k = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -74,7 +88,8 @@ __device__ bool group_sync_reduce(const SyncCtx& X, SyncShared<NDMAX>& sh, doubl
     if (t_arrive) *t_arrive = globaltimer_ns();
     __threadfence();
     atomicAdd(X.sync + g, 1ull);
-    target += static_cast<unsigned long long>(X.C);
+    const unsigned long long target = sh.target + static_cast<unsigned long long>(X.C);
+    sh.target = target;
     const unsigned long long t0 = globaltimer_ns();
     int ab = 0;
     while (ld_volatile_u64(X.sync + g) < target) {
@@ -91,10 +106,10 @@ __device__ bool group_sync_reduce(const SyncCtx& X, SyncShared<NDMAX>& sh, doubl
     }
     __threadfence();
     sh.abort = ab;
+    sh.bar_idx += 1;
   }
   __syncthreads();
   if (sh.abort) return false;
-  ++bar_idx;
   {
     const int t = threadIdx.x;
     const int s = t / (NDMAX * 32);

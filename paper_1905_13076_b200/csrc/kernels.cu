@@ -22,6 +22,7 @@
 #include "pppc_internal.h"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 
 namespace pppc {
@@ -141,6 +142,10 @@ __device__ __forceinline__ bool row_shared(const PropParams& P, int i) {
   return P.rowkind == nullptr || __ldg(P.rowkind + i) == 0;
 }
 
+__device__ __forceinline__ void refill_finish(const PropParams& P, int i, int sys, size_t vo, int step, bool first,
+                                              bool shared_row, double ku, double mr, double dval,
+                                              double (&acc)[kNDots]);
+
 template <int NPE>
 __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* curves, int i, int sys, size_t vo,
                                            size_t ao, int step, bool first, double (&acc)[kNDots]) {
@@ -185,10 +190,6 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
       }
     }
   }
-  // excitation f_i = sum_t c_t(t_next) pattern_t[i]  (proj/src/problem.cpp:52-63)
-  double f = 0.0;
-  const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
-  for (int t = 0; t < P.nterms; ++t) f += cf[t] * __ldg(P.pat + static_cast<size_t>(t) * P.d + i);
   // mass term M (u - u_prev)/dt, zero at the first Newton iterate of a step
   double mr = 0.0, dval = 0.0;
   const int dslot = __ldg(P.diag + i);
@@ -211,6 +212,19 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
     P.A[ao + static_cast<size_t>(k) * kLanes] = av;
     if (k == dslot) dval = av;
   }
+  refill_finish(P, i, sys, vo, step, first, shared_row, ku, mr, dval, acc);
+}
+
+// Row epilogue of the refill: excitation, residual R = M(u - u_prev)/dt + K(u)u
+// - f, Jacobi diagonal, r = -R, p = Dinv r, and the row's dot partials.
+__device__ __forceinline__ void refill_finish(const PropParams& P, int i, int sys, size_t vo, int step, bool first,
+                                              bool shared_row, double ku, double mr, double dval,
+                                              double (&acc)[kNDots]) {
+  const size_t iv = vo + static_cast<size_t>(i) * kLanes;
+  // excitation f_i = sum_t c_t(t_next) pattern_t[i]  (proj/src/problem.cpp:52-63)
+  double f = 0.0;
+  const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
+  for (int t = 0; t < P.nterms; ++t) f += cf[t] * __ldg(P.pat + static_cast<size_t>(t) * P.d + i);
   const double dinv = shared_row ? __ldg(P.Dsh + i) : 1.0 / dval;
   const double R = mr + ku - f;
   const double r = -R;
@@ -238,132 +252,38 @@ __device__ __forceinline__ void spmv_epilogue(const PropParams& P, int i, size_t
   acc[2] += qv * (di * qv);
 }
 
-// ---------------------------------------------------------------------------
-// TMA staging of CSR rows (nonlinear path, phase A).  Per warp, kStages
-// shared-memory stages each hold one row's per-system matrix values (up to
-// kStageSlots slots x 32 lanes), r and Dinv, filled by cp.async.bulk and
-// completed through an mbarrier (expect_tx).  One lane issues the copies
-// kStages rows ahead, so ~4 rows x 2.3 KB per warp are in flight without
-// holding registers; the lanes then read their values from shared memory.
-constexpr int kStages = 4;
-constexpr int kStageSlots = 8;
-struct StageBuf {
-  double a[kStageSlots][kLanes];
-  double r[kLanes];
-  double d[kLanes];
+// Per-phase base pointers.  opq() hides a kernel-parameter pointer from
+// loop-invariant code motion: without it the compiler hoists every base address
+// of both PCG phases out of the persistent interval loop and keeps them all in
+// registers, which the phase pipelines then lack (spills).
+template <class T>
+__device__ __forceinline__ T* opq(T* ptr) {
+  asm volatile("" : "+l"(ptr));
+  return ptr;
+}
+
+struct PhasePtrs {
+  const double* p;     // this lane's p (vo applied)
+  const double* r;
+  const double* dinv;
+  const double* A;     // this lane's per-system values (ao applied)
+  double* q;
+  const double* dsh;   // shared Jacobi / padded shared rows / rowkind flag
+  const double* ashe;
+  bool kinds;          // rows have kinds (element problems)
 };
-constexpr size_t kStageSmem = sizeof(StageBuf) * kStages * kWarps + sizeof(unsigned long long) * kStages * kWarps;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
-  unsigned ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// bounded: a staging protocol error traps (kernel error) instead of hanging the GPU
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  unsigned long long spins = 0;
-  while (!mbar_try_wait(bar, parity))
-    if (++spins > (1ull << 28)) __trap();
-}
-__device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-// generic-proxy global writes (made visible by the group barrier) must be
-// ordered before the async-proxy (TMA) reads of the same data
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-// One lane: stage row i (values of this group's 32 lanes, r, Dinv) into `b`.
-__device__ __forceinline__ void stage_row(const PropParams& P, int i, size_t gvb, size_t gab, StageBuf* b,
-                                          unsigned long long* bar) {
-  const int base = __ldg(P.rp + i), len = __ldg(P.rp + i + 1) - base;
-  if (len > kStageSlots) {  // long / irregular rows are read directly
-    mbar_expect_tx(bar, 0);
-    return;
-  }
-  const unsigned row_bytes = kLanes * sizeof(double);
-  mbar_expect_tx(bar, (len + 2) * row_bytes);
-  tma_load(&b->a[0][0], P.A + gab + static_cast<size_t>(base) * kLanes, len * row_bytes, bar);
-  tma_load(b->r, P.r + gvb + static_cast<size_t>(i) * kLanes, row_bytes, bar);
-  tma_load(b->d, P.Dinv + gvb + static_cast<size_t>(i) * kLanes, row_bytes, bar);
-}
-
-// Phase A with TMA-staged rows (nonlinear path).  Executed by every lane of a
-// warp that has any lane in phase A; `active` lanes compute.
-__device__ __forceinline__ void spmv_range_staged(const PropParams& P, int rb, int re, int stride, size_t vo,
-                                                  size_t ao, bool active, StageBuf* bufs, unsigned long long* bars,
-                                                  unsigned& cnt, unsigned& phases, double (&acc)[kNDots]) {
-  const int lane = threadIdx.x & 31;
-  const size_t gvb = vo - lane, gab = ao - lane;
-  const int n = rb < re ? (re - rb + stride - 1) / stride : 0;
-  if (lane == 0) fence_proxy_async_global();
-  for (int j = 0; j < kStages && j < n; ++j)
-    if (lane == 0) {
-      const unsigned s = (cnt + j) % kStages;
-      stage_row(P, rb + j * stride, gvb, gab, bufs + s, bars + s);
-    }
-  for (int j = 0; j < n; ++j) {
-    const int i = rb + j * stride;
-    const unsigned s = cnt % kStages;
-    const int base = __ldg(P.rp + i), len = __ldg(P.rp + i + 1) - base;
-    int cj[kStageSlots];
-#pragma unroll
-    for (int k = 0; k < kStageSlots; ++k) cj[k] = k < len ? __ldg(P.ci + base + k) : i;
-    mbar_wait(bars + s, (phases >> s) & 1u);
-    phases ^= 1u << s;
-    if (active && len <= kStageSlots) {
-      const StageBuf* b = bufs + s;
-      double pv[kStageSlots];
-#pragma unroll
-      for (int k = 0; k < kStageSlots; ++k) pv[k] = k < len ? P.p[vo + static_cast<size_t>(cj[k]) * kLanes] : 0.0;
-      double qv = 0.0;
-#pragma unroll
-      for (int k = 0; k < kStageSlots; ++k)
-        if (k < len) qv += b->a[k][lane] * pv[k];
-      const size_t iv = vo + static_cast<size_t>(i) * kLanes;
-      P.q[iv] = qv;
-      const double di = b->d[lane], ri = b->r[lane];
-      const double pi = P.p[iv];
-      const double zi = di * ri;
-      acc[0] += pi * qv;
-      acc[1] += qv * zi;
-      acc[2] += qv * (di * qv);
-    } else if (active && len <= kLongRow) {
-      double qv = 0.0;
-      for (int k = base; k < base + len; ++k)
-        qv += P.A[ao + static_cast<size_t>(k) * kLanes] * P.p[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes];
-      const size_t iv = vo + static_cast<size_t>(i) * kLanes;
-      P.q[iv] = qv;
-      const double di = P.Dinv[iv], pi = P.p[iv], ri = P.r[iv];
-      const double zi = di * ri;
-      acc[0] += pi * qv;
-      acc[1] += qv * zi;
-      acc[2] += qv * (di * qv);
-    }
-    __syncwarp();
-    if (lane == 0 && j + kStages < n) stage_row(P, rb + (j + kStages) * stride, gvb, gab, bufs + s, bars + s);
-    ++cnt;
-  }
+__device__ __forceinline__ PhasePtrs phase_ptrs(const PropParams& P, size_t vo, size_t ao) {
+  PhasePtrs Q;
+  Q.p = opq(P.p) + vo;
+  Q.r = opq(P.r) + vo;
+  Q.dinv = opq(P.Dinv) + vo;
+  Q.A = opq(P.A) + ao;
+  Q.q = opq(P.q) + vo;
+  Q.dsh = opq(P.Dsh);
+  Q.ashe = opq(P.AshE);
+  Q.kinds = P.rowkind != nullptr;
+  return Q;
 }
 
 // Phase A, one row: every load of row i is issued from its record (pppc_internal.h
@@ -381,98 +301,197 @@ struct RowData {
   double po, ro, dv;
 };
 
-__device__ __forceinline__ void issue_row(const PropParams& P, const int4* rec, int i, const double* pb,
-                                          const double* rb, const double* db, const double* Ab, RowData& o) {
-  const int4 h = rec[kRecInts4 * i];
-  const int4 c03 = rec[kRecInts4 * i + 1], c47 = rec[kRecInts4 * i + 2];
+__device__ __forceinline__ void issue_row(const PhasePtrs& Q, const int4* rec, int ri, int i, RowData& o) {
+  const int4 h = rec[kRecInts4 * ri];
+  const int4 c03 = rec[kRecInts4 * ri + 1], c47 = rec[kRecInts4 * ri + 2];
   o.base = h.x;
   o.len = h.y;
-  o.shared = P.rowkind == nullptr || h.z == 0;
+  o.shared = !Q.kinds || h.z == 0;
   const int c[kEll] = {c03.x, c03.y, c03.z, c03.w, c47.x, c47.y, c47.z, c47.w};
 #pragma unroll
-  for (int k = 0; k < kEll; ++k) o.pv[k] = pb[static_cast<ptrdiff_t>(c[k]) * kLanes];
+  for (int k = 0; k < kEll; ++k) o.pv[k] = Q.p[static_cast<ptrdiff_t>(c[k]) * kLanes];
   const size_t io = static_cast<size_t>(i) * kLanes;
-  o.po = pb[io];
-  o.ro = rb[io];
-  if (o.shared) {
-    o.dv = __ldg(P.Dsh + i);
-    const double2* ap = reinterpret_cast<const double2*>(P.AshE + static_cast<size_t>(i) * kEll);
+  o.po = Q.p[io];
+  o.ro = Q.r[io];
+  // branch-free: one pointer and stride select the shared or per-system copy
+  // (a branch here makes the compiler serialise the two load groups)
+  const double* dp = o.shared ? Q.dsh + i : Q.dinv + io;
+  o.dv = *dp;
+  const double* ap = o.shared ? Q.ashe + static_cast<size_t>(i) * kEll : Q.A + static_cast<size_t>(o.base) * kLanes;
+  const int as = o.shared ? 1 : kLanes;
+  const int n = o.shared ? kEll : (o.len <= kEll ? o.len : 0);
 #pragma unroll
-    for (int k = 0; k < kEll / 2; ++k) {
-      const double2 v = __ldg(ap + k);
-      o.a[2 * k] = v.x;
-      o.a[2 * k + 1] = v.y;
-    }
-  } else {
-    o.dv = db[io];
-    const int n = o.len <= kEll ? o.len : 0;
-    const double* ap = Ab + static_cast<size_t>(o.base) * kLanes;
-#pragma unroll
-    for (int k = 0; k < kEll; ++k) o.a[k] = k < n ? ap[k * kLanes] : 0.0;
-  }
+  for (int k = 0; k < kEll; ++k) o.a[k] = k < n ? ap[k * as] : 0.0;
 }
 
-// Row i of phase A from `cur` (issued one row earlier); issues row i1 into `nxt`.
+// L2 prefetch (no register or scoreboard cost) of the streamed operands of a
+// row a few rows ahead of its loads: the loads then see L2 rather than DRAM
+// latency, which is what bounds a warp with one row in flight.
+__device__ __forceinline__ void pf_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); }
+
+__device__ __forceinline__ void prefetch_row_a(const PhasePtrs& Q, const int4* rec, int ri, int i) {
+  const size_t io = static_cast<size_t>(i) * kLanes;
+  pf_l2(Q.r + io);
+  if (!Q.kinds) return;
+  const int4 h = rec[kRecInts4 * ri];
+  if (h.z == 0) return;
+  pf_l2(Q.dinv + io);
+  const double* ap = Q.A + static_cast<size_t>(h.x) * kLanes;
+  const int n = h.y <= kEll ? h.y : 0;
+#pragma unroll
+  for (int k = 0; k < kEll; ++k)
+    if (k < n) pf_l2(ap + k * kLanes);
+}
+
+// Row i of phase A from `cur` (issued one row earlier); issues row i1 (record
+// ri1) into `nxt`.
 template <bool LINEAR>
-__device__ __forceinline__ void spmv_row(const PropParams& P, const int4* rec, int i, int i1, bool more,
-                                         const double* pb, const double* rbp, const double* dbp, const double* Ab,
-                                         double* qb, const RowData& cur, RowData& nxt, double (&acc)[kNDots]) {
-  if (more) issue_row(P, rec, i1, pb, rbp, dbp, Ab, nxt);
+__device__ __forceinline__ void spmv_row(const PropParams& P, const PhasePtrs& Q, const int4* rec, int i, int ri1,
+                                         int i1, bool more, const RowData& cur, RowData& nxt,
+                                         double (&acc)[kNDots]) {
+  if (more) issue_row(Q, rec, ri1, i1, nxt);
   double qv = 0.0;
   if (cur.len <= kEll) {
 #pragma unroll
     for (int k = 0; k < kEll; ++k) qv += cur.a[k] * cur.pv[k];
   } else if (cur.len <= kLongRow) {
     for (int k = cur.base; k < cur.base + cur.len; ++k) {
-      const double av = cur.shared ? __ldg(P.Ash + k) : Ab[static_cast<size_t>(k) * kLanes];
-      qv += av * pb[static_cast<ptrdiff_t>(__ldg(P.ci + k)) * kLanes];
+      const double av = cur.shared ? __ldg(P.Ash + k) : Q.A[static_cast<size_t>(k) * kLanes];
+      qv += av * Q.p[static_cast<ptrdiff_t>(__ldg(P.ci + k)) * kLanes];
     }
   } else {
     return;  // long rows: spmv_long_rows
   }
-  qb[static_cast<size_t>(i) * kLanes] = qv;
+  Q.q[static_cast<size_t>(i) * kLanes] = qv;
   const double zi = cur.dv * cur.ro;
   acc[0] += cur.po * qv;
   acc[1] += qv * zi;
   acc[2] += qv * (cur.dv * qv);
 }
 
-// Phase A over a warp's rows (rb, rb + stride, ... < re): q = A p and the
-// partials p.q, q.z, q.Dq.  Unrolled by two so the in-flight and the consumed
-// operand sets keep fixed registers.
+// A warp's rows: row(j) = rb + j * stride (< re), record index ri0 + j * rstep.
+struct RowSeq {
+  int rb, re, stride, ri0, rstep;
+};
+
+// Phase A over a warp's rows: q = A p and the partials p.q, q.z, q.Dq.
+// Unrolled by two so the in-flight and the consumed operand sets keep fixed
+// registers.
 template <bool LINEAR>
-__device__ __forceinline__ void spmv_range(const PropParams& P, const int4* rec, int rb, int re, int stride,
-                                           size_t vo, size_t ao, double (&acc)[kNDots]) {
-  if (rb >= re) return;
-  const double* pb = P.p + vo;
-  const double* rbp = P.r + vo;
-  const double* dbp = P.Dinv + vo;
-  const double* Ab = P.A + ao;
-  double* qb = P.q + vo;
+__device__ __forceinline__ void spmv_range(const PropParams& P, const int4* rec, const RowSeq& S, size_t vo,
+                                           size_t ao, double (&acc)[kNDots]) {
+  if (S.rb >= S.re) return;
+  const PhasePtrs Q = phase_ptrs(P, vo, ao);
   RowData ra, rc;
-  issue_row(P, rec, rb, pb, rbp, dbp, Ab, ra);
-  for (int i = rb;;) {
-    int i1 = i + stride;
-    spmv_row<LINEAR>(P, rec, i, i1, i1 < re, pb, rbp, dbp, Ab, qb, ra, rc, acc);
-    if (i1 >= re) break;
-    i = i1;
-    i1 = i + stride;
-    spmv_row<LINEAR>(P, rec, i, i1, i1 < re, pb, rbp, dbp, Ab, qb, rc, ra, acc);
-    if (i1 >= re) break;
-    i = i1;
+  issue_row(Q, rec, S.ri0, S.rb, ra);
+  int ri = S.ri0;
+  const int pfd = P.pf_dist, pfs = pfd * S.stride, pfr = pfd * S.rstep;
+  for (int i = S.rb;;) {
+    if (pfd > 0 && i + pfs < S.re) prefetch_row_a(Q, rec, ri + pfr, i + pfs);
+    int i1 = i + S.stride, ri1 = ri + S.rstep;
+    spmv_row<LINEAR>(P, Q, rec, i, ri1, i1, i1 < S.re, ra, rc, acc);
+    if (i1 >= S.re) break;
+    i = i1, ri = ri1;
+    if (pfd > 0 && i + pfs < S.re) prefetch_row_a(Q, rec, ri + pfr, i + pfs);
+    i1 = i + S.stride, ri1 = ri + S.rstep;
+    spmv_row<LINEAR>(P, Q, rec, i, ri1, i1, i1 < S.re, rc, ra, acc);
+    if (i1 >= S.re) break;
+    i = i1, ri = ri1;
   }
 }
 
-// The block's row records in shared memory (P.rec_rows > 0), else the global
-// copy; the returned pointer is indexed by global row.
+// Row ownership: rows go in chunks of kWarps, chunk k to block
+// k mod C of the group, one row of a chunk per warp.  A group's C blocks thus
+// sweep every array together through one moving window (DRAM page locality of
+// a plain stream), and work per block is balanced to one chunk.  Warp w of
+// block c owns rows (c + j C) kWarps + w.  The block's row records are copied
+// to shared memory in that order when they fit (P.rec_rows > 0).
+__device__ __forceinline__ int first_chunk(const PropParams& P, int c) {
+  return (c - P.chunk_rot % P.C + P.C) % P.C;
+}
+
+__device__ __forceinline__ RowSeq warp_rows(const PropParams& P, int c, int warp) {
+  RowSeq S;
+  S.rb = first_chunk(P, c) * kWarps + warp;
+  S.re = P.d;
+  S.stride = P.C * kWarps;
+  if (P.rec_rows > 0) {
+    S.ri0 = warp;
+    S.rstep = kWarps;
+  } else {
+    S.ri0 = S.rb;
+    S.rstep = S.stride;
+  }
+  return S;
+}
+
 __device__ __forceinline__ const int4* stage_records(const PropParams& P, int c, int4* srec) {
   if (P.rec_rows <= 0) return P.rowrec;
-  const int r0 = P.warp_row_begin[c * kWarps], r1 = P.warp_row_begin[c * kWarps + kWarps];
-  const int n = (r1 - r0) * kRecInts4;
-  const int4* src = P.rowrec + static_cast<size_t>(r0) * kRecInts4;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) srec[t] = __ldg(src + t);
+  const int n = P.rec_rows * kRecInts4;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const int lr = t / kRecInts4, part = t - lr * kRecInts4;
+    const int row = (first_chunk(P, c) + (lr / kWarps) * P.C) * kWarps + (lr % kWarps);
+    if (row < P.d) srec[t] = __ldg(P.rowrec + static_cast<size_t>(row) * kRecInts4 + part);
+  }
   __syncthreads();
-  return srec - static_cast<ptrdiff_t>(r0) * kRecInts4;
+  return srec;
+}
+
+// Refill of the long rows this block owns (the polar hub: ntheta+1 slots),
+// called by every thread of the block.  For a shared-value row the K u and
+// mass sums are split across the 16 warps (4 slots in flight per warp) and
+// combined in fixed order; warp 0 finishes the row.  A long row with
+// per-system values falls back to the serial element loop on warp 0.
+// `active`: this lane refills in this interval.
+template <int NPE>
+__device__ __forceinline__ void refill_long_rows(const PropParams& P, const ps_curve* curves, bool active,
+                                                 bool first, int sys, size_t vo, size_t ao, int step, int c,
+                                                 double (*lpart)[32], double (*lpart2)[32],
+                                                 double (&acc)[kNDots]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = 0; j < P.n_long; ++j) {
+    if (__ldg(P.long_owner + j) != c) continue;
+    const int i = __ldg(P.long_rows + j);
+    if (!row_shared(P, i)) {
+      if (warp == 0 && active) refill_row<NPE>(P, curves, i, sys, vo, ao, step, first, acc);
+      continue;
+    }
+    const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+    const double* Kr = NPE == 0 ? P.Klin : P.Kc;
+    double kp = 0.0, mp = 0.0;
+    if (active) {
+      for (int k0 = base + warp; k0 < end; k0 += 4 * kWarps) {
+        double kv[4], mv[4], uv[4], up[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u * kWarps;
+          const bool ok = k < end;
+          const size_t jv = vo + static_cast<size_t>(ok ? __ldg(P.ci + k) : i) * kLanes;
+          kv[u] = ok ? __ldg(Kr + k) : 0.0;
+          mv[u] = ok ? __ldg(P.M + k) : 0.0;
+          uv[u] = ok ? P.u[jv] : 0.0;
+          up[u] = (ok && !first) ? P.uprev[jv] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          kp += kv[u] * uv[u];
+          if (!first) mp += mv[u] * ((uv[u] - up[u]) / P.dt);
+        }
+      }
+    }
+    lpart[warp][lane] = kp;
+    lpart2[warp][lane] = mp;
+    __syncthreads();
+    if (warp == 0 && active) {
+      double ku = 0.0, mr = 0.0;
+      for (int w = 0; w < kWarps; ++w) {
+        ku += lpart[w][lane];
+        mr += lpart2[w][lane];
+      }
+      refill_finish(P, i, sys, vo, step, first, true, ku, mr, 0.0, acc);
+    }
+    __syncthreads();
+  }
 }
 
 // Long rows (the polar hub: ntheta+1 slots) walked serially by one lane would
@@ -515,42 +534,67 @@ __device__ __forceinline__ void spmv_long_rows(const PropParams& P, bool active,
   }
 }
 
-// Phase B over a warp's row range, four rows per batch (all loads of a batch
-// issued together): x += alpha p (x = alpha p on the first iteration),
-// r -= alpha q, z = D r, p = z + beta p; partials r.r and r.z.
+// Phase B over a warp's rows: x += alpha p (x = alpha p on the first
+// iteration), r -= alpha q, z = D r, p = z + beta p; partials r.r and r.z.
+// Rows go in batches of four whose twenty loads are issued together.  (A
+// software pipeline one batch ahead halves phase B in the standalone probe but
+// spills inside the persistent kernel, where it is slower.)
+struct BatchB {
+  double dv[4], pv[4], qv[4], rv[4], xv[4];
+};
+
+__device__ __forceinline__ void load_batch_b(const PhasePtrs& Q, const int4* rec, const double* x, const RowSeq& S,
+                                             int i0, int r0, bool first, BatchB& o) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    // rows past the end re-read row i0 (valid addresses, results unused):
+    // unpredicated, branch-free loads keep all twenty in flight together
+    const int i = i0 + u * S.stride;
+    const bool ok = i < S.re;
+    const int ii = ok ? i : i0;
+    const int ri = ok ? r0 + u * S.rstep : r0;
+    const size_t io = static_cast<size_t>(ii) * kLanes;
+    const bool sh = !Q.kinds || rec[kRecInts4 * ri].z == 0;
+    const double* dp = sh ? Q.dsh + ii : Q.dinv + io;
+    o.dv[u] = *dp;
+    o.pv[u] = Q.p[io];
+    o.qv[u] = Q.q[io];
+    o.rv[u] = Q.r[io];
+    o.xv[u] = first ? 0.0 : x[io];
+  }
+}
+
+__device__ __forceinline__ void store_batch_b(const PhasePtrs& Q, double* x, const RowSeq& S, int i0, double alpha,
+                                              double beta, bool first, const BatchB& o, double (&acc)[kNDots]) {
+  double* pw = const_cast<double*>(Q.p);
+  double* rw = const_cast<double*>(Q.r);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int i = i0 + u * S.stride;
+    if (i >= S.re) break;
+    const size_t io = static_cast<size_t>(i) * kLanes;
+    x[io] = first ? alpha * o.pv[u] : o.xv[u] + alpha * o.pv[u];
+    const double r = o.rv[u] - alpha * o.qv[u];
+    const double z = o.dv[u] * r;
+    rw[io] = r;
+    pw[io] = z + beta * o.pv[u];
+    acc[0] += r * r;
+    acc[1] += r * z;
+  }
+}
+
 template <bool LINEAR>
-__device__ __forceinline__ void update_range(const PropParams& P, const int4* rec, double* x, int rb, int re,
-                                             int stride, size_t vo, double alpha, double beta, bool first,
+__device__ __forceinline__ void update_range(const PropParams& P, const int4* rec, double* x, const RowSeq& S,
+                                             size_t vo, double alpha, double beta, bool first,
                                              double (&acc)[kNDots]) {
-  constexpr int B = 4;
-  for (int i0 = rb; i0 < re; i0 += B * stride) {
-    double dv[B], pv[B], qv[B], rv[B], xv[B];
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int i = i0 + u * stride;
-      const bool ok = i < re;
-      const int ii = ok ? i : i0;
-      const size_t iv = vo + static_cast<size_t>(ii) * kLanes;
-      const bool sh = P.rowkind == nullptr || rec[kRecInts4 * ii].z == 0;
-      dv[u] = ok ? (sh ? __ldg(P.Dsh + ii) : P.Dinv[iv]) : 0.0;
-      pv[u] = ok ? P.p[iv] : 0.0;
-      qv[u] = ok ? P.q[iv] : 0.0;
-      rv[u] = ok ? P.r[iv] : 0.0;
-      xv[u] = (ok && !first) ? x[iv] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int i = i0 + u * stride;
-      if (i >= re) break;
-      const size_t iv = vo + static_cast<size_t>(i) * kLanes;
-      x[iv] = first ? alpha * pv[u] : xv[u] + alpha * pv[u];
-      const double r = rv[u] - alpha * qv[u];
-      const double z = dv[u] * r;
-      P.r[iv] = r;
-      P.p[iv] = z + beta * pv[u];
-      acc[0] += r * r;
-      acc[1] += r * z;
-    }
+  if (S.rb >= S.re) return;
+  const PhasePtrs Q = phase_ptrs(P, vo, 0);
+  double* xb = opq(x) + vo;
+  const int bstep = 4 * S.stride, rstep = 4 * S.rstep;
+  for (int i0 = S.rb, r0 = S.ri0; i0 < S.re; i0 += bstep, r0 += rstep) {
+    BatchB ba;
+    load_batch_b(Q, rec, xb, S, i0, r0, first, ba);
+    store_batch_b(Q, xb, S, i0, alpha, beta, first, ba, acc);
   }
 }
 
@@ -570,15 +614,16 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   // the SpMV pipeline needs.)
   __shared__ Lane lanes[32];
   __shared__ int lact[32], lstep[32];
+  __shared__ int any_a;  // some lane of the block runs phase A in this interval
+  __shared__ int any_r;  // ... or a refill
+  __shared__ double lpart2[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x / P.C, c = blockIdx.x % P.C;
   const int sl = lane;
   const int sys = g * P.L + sl;
   const bool valid = (sl < P.L) && (sys < P.count);
-  const size_t vo = static_cast<size_t>(g) * P.d * kLanes + sl;
-  const size_t ao = static_cast<size_t>(g) * P.nnz * kLanes + sl;
   if (threadIdx.x < P.ncurves) sh_curves[threadIdx.x] = P.curves[threadIdx.x];
-  if (threadIdx.x == 0) sh.abort = 0;
+  sync_state_init(sh);
   if (warp == 0) {
     Lane& s = lanes[lane];
     s.alive = valid;
@@ -598,56 +643,67 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     s.max_nit = s.max_pit = s.last_nit = 0;
     lact[lane] = valid ? (LINEAR ? ACT_L0 : ACT_R0) : ACT_IDLE;
     lstep[lane] = 0;
+    if (lane == 0) any_a = 0, any_r = !LINEAR;
   }
   __syncthreads();
   extern __shared__ __align__(16) int4 srec[];
-  const int4* rec = stage_records(P, c, srec);
-  SyncCtx X;
-  X.sync = P.sync;
-  X.partials = P.partials;
-  X.abort_flag = P.abort_flag;
-  X.G = P.G;
-  X.C = P.C;
-  X.Lp = 32;
-  // rows of the block's range interleaved across its warps (row = begin + warp +
-  // 16 k): the warps sweep one contiguous window together and the streamed
-  // arrays are read in contiguous windows
-  const int row_begin = P.warp_row_begin[c * kWarps] + warp;
-  const int row_end = P.warp_row_begin[c * kWarps + kWarps];
-  unsigned long long target = 0;
-  int bar_idx = 0;
+  stage_records(P, c, srec);
   const bool writer = (c == 0) && (warp == 0) && valid;
-
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
-  long long lockstep = 0;
+  // Loop-carried state is kept minimal (barrier state and counters in shared
+  // memory, addresses recomputed per interval from g, c, warp, lane) so the
+  // phase pipelines get the registers.
+  __shared__ unsigned long long t_start, t_arr;  // debug timing (thread 0)
   // optional per-block timing (P.dbg): work / barrier-wait ns and counts for
   // intervals where lane 0 ran phase A, phase B, or anything else
-  __shared__ unsigned long long dbg[9];
-  if (threadIdx.x < 9) dbg[threadIdx.x] = 0;
+  // plus per-action lane-interval counts (dbg[9 + action])
+  __shared__ unsigned long long dbg[kDbgSlots];
+  if (threadIdx.x < kDbgSlots) dbg[threadIdx.x] = 0;
 
-  while (__syncthreads_or(lact[sl] != ACT_IDLE)) {
+  // One barrier interval.  Phase A only ever runs on even intervals and B on
+  // odd ones (ACT_WAIT alignment), so the loop is unrolled by two with the
+  // parity static: each copy contains only one PCG phase, and the register
+  // allocator never sees both phase pipelines live in one region.
+  bool aborted = false;
+  auto interval = [&](auto odd_tag) -> bool {
+    constexpr bool ODD = decltype(odd_tag)::value;
+    if (!__syncthreads_or(lact[sl] != ACT_IDLE)) return false;
     const int act = lact[sl];
     const int step = lstep[sl];
-    unsigned long long t_start = 0, t_arr = 0;
     if (P.dbg && threadIdx.x == 0) t_start = globaltimer_ns();
     const int dbg_kind = act == ACT_A ? 0 : (act == ACT_B ? 1 : 2);
     double* xs = LINEAR ? ((step & 1) ? P.ubuf0 : P.ubuf1) : P.x;
+    // per-interval addressing from opaque copies of (g, c, warp, lane): the
+    // compiler cannot hoist it and keep it live across the whole loop
+    int gq = g, cq = c, wq = warp, lq = sl;
+    asm volatile("" : "+r"(gq), "+r"(cq), "+r"(wq), "+r"(lq));
+    const size_t vo = static_cast<size_t>(gq) * P.d * kLanes + lq;
+    const size_t ao = static_cast<size_t>(gq) * P.nnz * kLanes + lq;
+    const RowSeq S = warp_rows(P, cq, wq);
+    const int row_begin = S.rb, row_end = S.re, row_step = S.stride;
+    const int4* rec = P.rec_rows > 0 ? static_cast<const int4*>(srec) : P.rowrec;
     // ------------------------------------------------ this lane's action
-    if (P.n_long > 0) spmv_long_rows<LINEAR>(P, act == ACT_A, vo, ao, c, lpart, acc);
+    if (P.n_long > 0 && any_a) spmv_long_rows<LINEAR>(P, act == ACT_A, vo, ao, c, lpart, acc);
+    if (!LINEAR)
+      if (P.n_long > 0 && any_r)
+        refill_long_rows<NPE>(P, sh_curves, act == ACT_R0 || act == ACT_R, act == ACT_R0, sys, vo, ao, step, c,
+                              lpart, lpart2, acc);
     if (act == ACT_A) {
-      spmv_range<LINEAR>(P, rec, row_begin, row_end, kWarps, vo, ao, acc);
+      if constexpr (!ODD) spmv_range<LINEAR>(P, rec, S, vo, ao, acc);
     } else if (act == ACT_B) {
-      update_range<LINEAR>(P, rec, xs, row_begin, row_end, kWarps, vo, lanes[sl].alpha, lanes[sl].beta,
-                           lanes[sl].pit == 0, acc);
+      if constexpr (ODD)
+        update_range<LINEAR>(P, rec, xs, S, vo, lanes[sl].alpha, lanes[sl].beta, lanes[sl].pit == 0, acc);
     } else if (act == ACT_R0 || act == ACT_R) {
-      if constexpr (!LINEAR)
-        for (int i = row_begin; i < row_end; i += kWarps)
+      if (!LINEAR)
+        for (int i = row_begin; i < row_end; i += row_step) {
+          if (P.n_long > 0 && __ldg(P.rp + i + 1) - __ldg(P.rp + i) > kLongRow) continue;  // refill_long_rows
           refill_row<NPE>(P, sh_curves, i, sys, vo, ao, step, act == ACT_R0, acc);
+        }
     } else if (act == ACT_U) {
       if (!lanes[sl].zero_dx) {
         const bool bt = lanes[sl].bt;
         const double lambda = lanes[sl].lambda;
-        for (int i = row_begin; i < row_end; i += kWarps) {
+        for (int i = row_begin; i < row_end; i += row_step) {
           // trial u += lambda delta (propagators.cpp:46-48), or a backtrack
           // u -= lambda delta with lambda already halved; delta must be finite
           const size_t iv = vo + static_cast<size_t>(i) * kLanes;
@@ -664,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       // b = M (u/dt) + f, x = 0, r = b, p = D b (proj/src/propagators.cpp:85-94)
       const double* uin = (step & 1) ? P.ubuf1 : P.ubuf0;
       const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
-      for (int i = row_begin; i < row_end; i += kWarps) {
+      for (int i = row_begin; i < row_end; i += row_step) {
         const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
         double mv = 0.0;
         for (int k = base; k < end; ++k)
@@ -683,14 +739,20 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     } else if (act == ACT_LU) {
       // the step solution must be finite (propagators.cpp:92); x0 = 0 when b = 0
       const bool zero = lanes[sl].pit == 0;
-      for (int i = row_begin; i < row_end; i += kWarps) {
+      for (int i = row_begin; i < row_end; i += row_step) {
         const size_t iv = vo + static_cast<size_t>(i) * kLanes;
         if (zero) xs[iv] = 0.0;
         acc[0] += isfinite(xs[iv]) ? 0.0 : 1.0;
       }
     }
-    if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, target, bar_idx, P.dbg ? &t_arr : nullptr)) return;
-    ++lockstep;
+    {
+      const SyncCtx X{P.sync, P.partials, P.abort_flag, P.G, P.C, 32};
+      if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, P.dbg ? &t_arr : nullptr)) {
+        aborted = true;
+        return false;
+      }
+    }
+    if (P.dbg && warp == 0 && valid) atomicAdd(&dbg[9 + act], 1ull);
     if (P.dbg && threadIdx.x == 0) {
       const unsigned long long t_end = globaltimer_ns();
       dbg[3 * dbg_kind + 0] += t_arr - t_start;
@@ -810,12 +872,23 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
           break;
       }
       if (!s.alive) a = ACT_IDLE;
-      if (a == ACT_A && (lockstep & 1)) a = ACT_WAIT;  // phase A only on even intervals
+      if (a == ACT_A && (sh.bar_idx & 1)) a = ACT_WAIT;  // phase A only on even intervals
       lact[lane] = a;
       lstep[lane] = stp;
+      const unsigned am = __ballot_sync(0xffffffffu, a == ACT_A);
+      const unsigned rm = __ballot_sync(0xffffffffu, a == ACT_R0 || a == ACT_R);
+      if (lane == 0) any_a = am != 0u, any_r = rm != 0u;
     }
     __syncthreads();
+    return true;
+  };
+  using EvenTag = std::integral_constant<bool, false>;
+  using OddTag = std::integral_constant<bool, true>;
+  for (;;) {
+    if (!interval(EvenTag())) break;
+    if (!interval(OddTag())) break;
   }
+  if (aborted) return;
 
   if (writer) {
     const Lane& s = lanes[lane];
@@ -830,43 +903,58 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     o.max_pcg = s.max_pit;
     P.out[sys] = o;
   }
-  if (c == 0 && threadIdx.x == 0) P.lockstep[g] = lockstep;
+  if (c == 0 && threadIdx.x == 0) P.lockstep[g] = sh.bar_idx;
+  __syncthreads();
   if (P.dbg && threadIdx.x == 0)
-    for (int k = 0; k < 9; ++k) P.dbg[static_cast<size_t>(blockIdx.x) * 9 + k] = dbg[k];
+    for (int k = 0; k < kDbgSlots; ++k) P.dbg[static_cast<size_t>(blockIdx.x) * kDbgSlots + k] = dbg[k];
 }
 
 // ------------------------------------------------------- phase probes
 // One PCG phase over the whole batch with the propagation kernel's exact thread
 // -> (group, row, lane) mapping and code, but no barriers or state machine:
 // a normal (non-cooperative) kernel that ncu can replay and that isolates the
-// memory behaviour of one phase.  mode 0: phase A (TMA-staged SpMV), 1: phase A
-// (register-pipelined SpMV), 2: phase B (update).  Dots go to `sink`.
+// memory behaviour of one phase.  mode 1: phase A (SpMV + dots), 2: phase B
+// (update), 3: phase B's streams as a flat grid-stride copy (the streaming
+// reference).  Dots go to `sink`.
 __global__ void __launch_bounds__(kThreads, 1) phase_probe_kernel(const PropParams P, int mode, double* sink) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x / P.C, c = blockIdx.x % P.C;
   const size_t vo = static_cast<size_t>(g) * P.d * kLanes + lane;
   const size_t ao = static_cast<size_t>(g) * P.nnz * kLanes + lane;
-  extern __shared__ __align__(128) unsigned char dsmem[];
-  StageBuf* bufs = reinterpret_cast<StageBuf*>(dsmem) + warp * kStages;
-  unsigned long long* bars =
-      reinterpret_cast<unsigned long long*>(dsmem + sizeof(StageBuf) * kStages * kWarps) + warp * kStages;
-  unsigned cnt = 0, phases = 0;
-  if (mode == 0 && lane == 0) {
-    for (int s2 = 0; s2 < kStages; ++s2) mbar_init(bars + s2, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-  const int row_begin = P.warp_row_begin[c * kWarps] + warp;
-  const int row_end = P.warp_row_begin[c * kWarps + kWarps];
-  const int4* rec = mode == 0 ? P.rowrec : stage_records(P, c, reinterpret_cast<int4*>(dsmem));
+  extern __shared__ __align__(16) int4 srec[];
+  const int4* rec = stage_records(P, c, srec);
+  const RowSeq S = warp_rows(P, c, warp);
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
-  if (mode == 0)
-    spmv_range_staged(P, row_begin, row_end, kWarps, vo, ao, true, bufs, bars, cnt, phases, acc);
-  else if (mode == 1)
-    spmv_range<false>(P, rec, row_begin, row_end, kWarps, vo, ao, acc);
-  else
-    update_range<false>(P, rec, P.x, row_begin, row_end, kWarps, vo, 1e-30, 1e-30, false, acc);
+  if (mode == 1)
+    spmv_range<false>(P, rec, S, vo, ao, acc);
+  else if (mode == 2)
+    update_range<false>(P, rec, P.x, S, vo, 1e-30, 1e-30, false, acc);
+  else {
+    // mode 3: the phase-B streams (5 reads, 3 writes) as a flat grid-stride
+    // loop over the whole padded batch: the streaming reference for mode 2
+    const size_t n = static_cast<size_t>(P.G) * P.d * kLanes;
+    const size_t nt = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t e0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e0 < n; e0 += 4 * nt) {
+      double dv[4], pv[4], qv[4], rv[4], xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t e = e0 + u * nt < n ? e0 + u * nt : e0;
+        dv[u] = P.Dinv[e], pv[u] = P.p[e], qv[u] = P.q[e], rv[u] = P.r[e], xv[u] = P.x[e];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t e = e0 + u * nt;
+        if (e >= n) break;
+        const double r = rv[u] - 1e-30 * qv[u];
+        const double z = dv[u] * r;
+        P.x[e] = xv[u] + 1e-30 * pv[u];
+        P.r[e] = r;
+        P.p[e] = z + 1e-30 * pv[u];
+        acc[0] += r * r;
+        acc[1] += r * z;
+      }
+    }
+  }
   if (acc[0] == 12345.0) sink[blockIdx.x] = acc[1] + acc[2];  // keep the dots live
 }
 
@@ -1093,7 +1181,7 @@ void launch_eval_curve(const ps_curve& c, int n, const double* b2, double* nu, d
 }
 
 int launch_phase_probe(const PropParams& prm, int mode, double* sink, cudaStream_t st) {
-  const size_t smem = std::max(kStageSmem, static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4));
+  const size_t smem = static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4);
   if (cudaFuncSetAttribute(reinterpret_cast<const void*>(phase_probe_kernel),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
     return PS_ERR_CUDA;

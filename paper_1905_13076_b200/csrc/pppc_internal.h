@@ -17,6 +17,7 @@ constexpr int kThreads = kWarps * 32;  // 512
 constexpr int kMaxCurves = 8;
 constexpr int kMaxTerms = 16;
 constexpr int kNDots = 4;
+constexpr int kDbgSlots = 18;          // debug timing: 9 timing words + 9 action counts
 constexpr int kRegularRow = 7;         // rows with <= 7 slots (the P1 polar mesh) use register accumulators
 constexpr int kLongRow = 32;           // rows with > 32 slots are split across a block's warps
 // Row records: rowrec[3i] = {first slot, length, kind (1 = per-system values),
@@ -56,6 +57,8 @@ struct PropParams {
   const int* diag;
   const int4* rowrec;   // [d][kRecInts4]
   int rec_rows;          // >0: largest block row range; records are staged in shared memory
+  int chunk_rot;         // chunk k of kWarps rows belongs to block (k + chunk_rot) mod C
+  int pf_dist;           // phase-A L2 prefetch distance in rows; 0 = off
   const double* M;
   const double* Klin;     // linear K (Newton on a linear problem)
   // shared step matrix M/dt + K (linear problems) or M/dt + K_const (element
@@ -106,7 +109,7 @@ struct PropParams {
   SysOut* out;                // [count]
   double* trace;              // [count][newton_max] or null
   int64_t* lockstep;          // [G] lock-step PCG iterations executed
-  unsigned long long* dbg;    // optional [G*C][9] timing (PPPC_DEBUG_TIMING)
+  unsigned long long* dbg;    // optional [G*C][kDbgSlots] timing (PPPC_DEBUG_TIMING)
 };
 
 struct DftPlan;

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
   const int sub = lane / P.Lp, sl = lane % P.Lp;
   const int h = g * P.L + sl;
   const bool valid = (sl < P.L) && (h < P.H);
-  if (threadIdx.x == 0) sh.abort = 0;
+  sync_state_init(sh);
   __syncthreads();
   SyncCtx X;
   X.sync = P.sync;
@@ -97,8 +97,6 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
   X.Lp = P.Lp;
   const int row_begin = P.warp_row_begin[c * kWarps + warp];
   const int row_end = P.warp_row_begin[c * kWarps + warp + 1];
-  unsigned long long target = 0;
-  int bar_idx = 0;
   const size_t H = static_cast<size_t>(P.H);
   const double2 s_b = valid ? P.shift[h] : make_double2(0.0, 0.0);
   double acc[kCND] = {0, 0, 0, 0, 0, 0};
@@ -127,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
       acc[1] += rz.y;
       acc[2] += bv.x * bv.x + bv.y * bv.y;
     }
-  if (!group_sync_reduce<kCND, 3>(X, sh, acc, g, c, target, bar_idx)) return;
+  if (!group_sync_reduce<kCND, 3>(X, sh, acc, g, c)) return;
   if (s.alive) {
     s.rho = make_double2(sh.tot[0][sl], sh.tot[1][sl]);
     const double bb = sh.tot[2][sl];
@@ -213,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
         acc[4] += qdq.x;
         acc[5] += qdq.y;
       }
-    if (!group_sync_reduce<kCND, 6>(X, sh, acc, g, c, target, bar_idx)) return;
+    if (!group_sync_reduce<kCND, 6>(X, sh, acc, g, c)) return;
     ++lockstep;
     if (s.act) {
       const double2 mu = make_double2(sh.tot[0][sl], sh.tot[1][sl]);
@@ -247,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
         acc[1] += rz.x;
         acc[2] += rz.y;
       }
-    if (!group_sync_reduce<kCND, 3>(X, sh, acc, g, c, target, bar_idx)) return;
+    if (!group_sync_reduce<kCND, 3>(X, sh, acc, g, c)) return;
     if (s.act) {
       const double rr = sh.tot[0][sl];
       s.rho = make_double2(sh.tot[1][sl], sh.tot[2][sl]);

@@ -17,7 +17,7 @@ import paper_1905_13076_b200 as ps  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=20)
-ap.add_argument("--mode", type=int, nargs="*", default=[0, 1, 2])
+ap.add_argument("--mode", type=int, nargs="*", default=[1, 2, 3])
 ap.add_argument("--nr", type=int, default=200)
 ap.add_argument("--ntheta", type=int, default=256)
 ap.add_argument("--N", type=int, default=100)
