@@ -507,6 +507,7 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.diag = P.diag;
   K.rowrec = P.rowrec;
   K.chunk_rot = chunk_rotation();
+  K.hub_split = (geo.n_long == 1 && std::getenv("PPPC_NO_HUB_SPLIT") == nullptr) ? 1 : 0;
   {
     // phase-A L2 prefetch distance in rows, PPPC_PF (default 0 = off: it helps
     // the standalone phase probe but not the persistent kernel)
@@ -627,7 +628,7 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
         std::fprintf(stderr,
                      "[pppc timing] %s: %.0f intervals/block, work %.2f us (block min %.2f max %.2f), wait %.2f us\n",
                      names[kind], n / nblk, work / n / 1e3, wmin / 1e3, wmax / 1e3, wait / n / 1e3);
-      if (kind < 2 && std::getenv("PPPC_DEBUG_BLOCKS")) {
+      if (std::getenv("PPPC_DEBUG_BLOCKS")) {
         std::fprintf(stderr, "[pppc blocks %s]", names[kind]);
         for (int b = 0; b < nblk; ++b) {
           const double cnt = static_cast<double>(h[b * W + 3 * kind + 2]);

@@ -313,15 +313,22 @@ __device__ __forceinline__ void issue_row(const PhasePtrs& Q, const int4* rec, i
   const size_t io = static_cast<size_t>(i) * kLanes;
   o.po = Q.p[io];
   o.ro = Q.r[io];
-  // branch-free: one pointer and stride select the shared or per-system copy
-  // (a branch here makes the compiler serialise the two load groups)
-  const double* dp = o.shared ? Q.dsh + i : Q.dinv + io;
-  o.dv = *dp;
-  const double* ap = o.shared ? Q.ashe + static_cast<size_t>(i) * kEll : Q.A + static_cast<size_t>(o.base) * kLanes;
-  const int as = o.shared ? 1 : kLanes;
-  const int n = o.shared ? kEll : (o.len <= kEll ? o.len : 0);
+  if (o.shared) {
+    o.dv = __ldg(Q.dsh + i);
+    const double2* ap = reinterpret_cast<const double2*>(Q.ashe + static_cast<size_t>(i) * kEll);
 #pragma unroll
-  for (int k = 0; k < kEll; ++k) o.a[k] = k < n ? ap[k * as] : 0.0;
+    for (int k = 0; k < kEll / 2; ++k) {
+      const double2 v = __ldg(ap + k);
+      o.a[2 * k] = v.x;
+      o.a[2 * k + 1] = v.y;
+    }
+  } else {
+    o.dv = Q.dinv[io];
+    const int n = o.len <= kEll ? o.len : 0;
+    const double* ap = Q.A + static_cast<size_t>(o.base) * kLanes;
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) o.a[k] = k < n ? ap[k * kLanes] : 0.0;
+  }
 }
 
 // L2 prefetch (no register or scoreboard cost) of the streamed operands of a
@@ -492,6 +499,25 @@ __device__ __forceinline__ void refill_long_rows(const PropParams& P, const ps_c
     }
     __syncthreads();
   }
+}
+
+// The single long row (P.hub_split) in phase A: its slots are dealt to the
+// group's C blocks (slot s to block s mod C, warp (s / C) mod kWarps), each
+// thread adding its slots' A p products into partial slot 3 of the phase-A
+// reduction.  The group barrier then sums the row's q in fixed order and the
+// transitions finish it, so no block carries the 1 + ntheta slot row alone.
+__device__ __forceinline__ void hub_partial(const PropParams& P, size_t vo, size_t ao, int c, int warp,
+                                            double (&acc)[kNDots]) {
+  const int i = __ldg(P.long_rows);
+  const int base = __ldg(P.rp + i), len = __ldg(P.rp + i + 1) - base;
+  const bool sh = row_shared(P, i);
+  double part = 0.0;
+  for (int sidx = c + P.C * warp; sidx < len; sidx += P.C * kWarps) {
+    const int k = base + sidx;
+    const double av = sh ? __ldg(P.Ash + k) : P.A[ao + static_cast<size_t>(k) * kLanes];
+    part += av * P.p[vo + static_cast<size_t>(__ldg(P.ci + k)) * kLanes];
+  }
+  acc[3] += part;
 }
 
 // Long rows (the polar hub: ntheta+1 slots) walked serially by one lane would
@@ -683,7 +709,13 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     const int row_begin = S.rb, row_end = S.re, row_step = S.stride;
     const int4* rec = P.rec_rows > 0 ? static_cast<const int4*>(srec) : P.rowrec;
     // ------------------------------------------------ this lane's action
-    if (P.n_long > 0 && any_a) spmv_long_rows<LINEAR>(P, act == ACT_A, vo, ao, c, lpart, acc);
+    if (P.n_long > 0 && any_a) {
+      if (P.hub_split) {
+        if (act == ACT_A) hub_partial(P, vo, ao, cq, wq, acc);
+      } else {
+        spmv_long_rows<LINEAR>(P, act == ACT_A, vo, ao, c, lpart, acc);
+      }
+    }
     if (!LINEAR)
       if (P.n_long > 0 && any_r)
         refill_long_rows<NPE>(P, sh_curves, act == ACT_R0 || act == ACT_R, act == ACT_R0, sys, vo, ao, step, c,
@@ -765,7 +797,21 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       int a = act;
       int stp = step;
       const double t_now = (a != ACT_IDLE) ? P.t_next[static_cast<size_t>(stp) * P.count + sys] : 0.0;
-      const double t0v = sh.tot[0][sl], t1v = sh.tot[1][sl], t2v = sh.tot[2][sl], t3v = sh.tot[3][sl];
+      double t0v = sh.tot[0][sl], t1v = sh.tot[1][sl], t2v = sh.tot[2][sl];
+      const double t3v = sh.tot[3][sl];
+      if (a == ACT_A && P.hub_split) {
+        // the single long row's q came through the reduction (slot 3): add its
+        // terms to p.q, q.z, q.Dq here, identically in every block; the owner
+        // stores it for phase B
+        const int hub = __ldg(P.long_rows);
+        const size_t ih = static_cast<size_t>(g) * P.d * kLanes + sl + static_cast<size_t>(hub) * kLanes;
+        const double qh = t3v, ph = P.p[ih], rh = P.r[ih];
+        const double dh = row_shared(P, hub) ? __ldg(P.Dsh + hub) : P.Dinv[ih];
+        t0v += ph * qh;
+        t1v += qh * (dh * rh);
+        t2v += qh * (dh * qh);
+        if (c == __ldg(P.long_owner)) P.q[ih] = qh;
+      }
       switch (a) {
         case ACT_R0: {
           s.tol = P.newton_tol_abs + P.newton_tol_rel * sqrt(t1v);

@@ -59,6 +59,7 @@ struct PropParams {
   int rec_rows;          // >0: largest block row range; records are staged in shared memory
   int chunk_rot;         // chunk k of kWarps rows belongs to block (k + chunk_rot) mod C
   int pf_dist;           // phase-A L2 prefetch distance in rows; 0 = off
+  int hub_split;         // 1: the single long row's phase-A product goes through the reduction
   const double* M;
   const double* Klin;     // linear K (Newton on a linear problem)
   // shared step matrix M/dt + K (linear problems) or M/dt + K_const (element
