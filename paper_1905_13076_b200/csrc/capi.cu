@@ -327,6 +327,19 @@ void build_problem(ps_ctx* ctx, const ps_problem_desc* desc) {
       rec[kRecInts4 * i + 2] = make_int4(c[4], c[5], c[6], c[7]);
     }
     P.rowrec = upload(rec.data(), rec.size(), "row records");
+    // padded per-row mass and shared stiffness values (refill of rows <= kEll)
+    std::vector<double> me(static_cast<size_t>(P.d) * kEll, 0.0), ke(static_cast<size_t>(P.d) * kEll, 0.0);
+    const std::vector<double>& Kref = P.linear ? P.h_K : P.h_Kc;
+    for (int i = 0; i < P.d; ++i) {
+      const int b = P.h_rp[i], len = P.h_rp[i + 1] - b;
+      if (len > kEll) continue;
+      for (int k = 0; k < len; ++k) {
+        me[static_cast<size_t>(i) * kEll + k] = P.h_M[b + k];
+        ke[static_cast<size_t>(i) * kEll + k] = Kref[b + k];
+      }
+    }
+    P.ME = upload(me.data(), me.size(), "padded mass rows");
+    P.KE = upload(ke.data(), ke.size(), "padded stiffness rows");
   }
   P.nterms = desc->n_terms;
   P.period = desc->period;
@@ -506,6 +519,8 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.ci = P.ci;
   K.diag = P.diag;
   K.rowrec = P.rowrec;
+  K.ME = P.ME;
+  K.KE = P.KE;
   K.chunk_rot = chunk_rotation();
   K.hub_split = (geo.n_long == 1 && std::getenv("PPPC_NO_HUB_SPLIT") == nullptr) ? 1 : 0;
   {
@@ -611,7 +626,7 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
     check(cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream), "dbg");
     check(cudaStreamSynchronize(ctx->stream), "dbg");
     cudaFree(dbg);
-    const char* names[3] = {"A", "B", "other"};
+    const char* names[3] = {"A (no refill)", "B+other (no refill)", "with refill"};
     for (int kind = 0; kind < 3; ++kind) {
       double work = 0, wait = 0, wmin = 1e300, wmax = 0, n = 0;
       for (int b = 0; b < nblk; ++b) {
@@ -867,7 +882,7 @@ int ps_create(const ps_problem_desc* problem, const ps_time_mesh* mesh, const ps
 void ps_destroy(ps_ctx* ctx) {
   if (!ctx) return;
   DevProblem& P = ctx->P;
-  void* ptrs[] = {P.rowrec, P.rowkind, P.Kc, P.rp, P.ci, P.diag, P.M, P.K, P.adj_ptr, P.adj, P.adj_rel, P.en, P.eS, P.einvA, P.ecurve,
+  void* ptrs[] = {P.rowrec, P.ME, P.KE, P.rowkind, P.Kc, P.rp, P.ci, P.diag, P.M, P.K, P.adj_ptr, P.adj, P.adj_rel, P.en, P.eS, P.einvA, P.ecurve,
                   P.pat, ctx->u, ctx->uprev, ctx->x, ctx->r, ctx->p, ctx->q, ctx->Dinv, ctx->A, ctx->io_a,
                   ctx->io_b, ctx->sync, ctx->partials, ctx->abort_flag, ctx->out, ctx->trace, ctx->lockstep,
                   ctx->coef, ctx->tnext};

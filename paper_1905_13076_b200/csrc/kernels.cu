@@ -149,7 +149,6 @@ __device__ __forceinline__ void refill_finish(const PropParams& P, int i, int sy
 template <int NPE>
 __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* curves, int i, int sys, size_t vo,
                                            size_t ao, int step, bool first, double (&acc)[kNDots]) {
-  const size_t iv = vo + static_cast<size_t>(i) * kLanes;
   const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
   const int len = end - base;
   const bool regular = len <= kRegularRow;
@@ -213,6 +212,109 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
     if (k == dslot) dval = av;
   }
   refill_finish(P, i, sys, vo, step, first, shared_row, ku, mr, dval, acc);
+}
+
+// refill_row for a row of <= kEll slots, driven by its record (pppc_internal.h):
+// the row's u and u_prev entries are gathered in one go (the element nodes of
+// every element adjacent to row i are columns of row i, so the element loop
+// reads them from the warp's shared-memory slot scratch `us` through adj_rel
+// instead of chasing element -> node -> u), the padded mass / shared stiffness
+// rows come as uniform loads.  Same arithmetic, same order as refill_row.
+template <int NPE>
+__device__ __forceinline__ void refill_row_ell(const PropParams& P, const ps_curve* curves, const int4* rec, int ri,
+                                               int i, int sys, size_t vo, size_t ao, int step, bool first,
+                                               double (*us)[32], double (&acc)[kNDots]) {
+  const int lane = threadIdx.x & 31;
+  const int4 h = rec[kRecInts4 * ri];
+  const int4 c03 = rec[kRecInts4 * ri + 1], c47 = rec[kRecInts4 * ri + 2];
+  const int base = h.x, len = h.y;
+  const bool shared_row = P.rowkind == nullptr || h.z == 0;
+  const int c[kEll] = {c03.x, c03.y, c03.z, c03.w, c47.x, c47.y, c47.z, c47.w};
+  // the row's u entries go to the lane's scratch column right away (few
+  // registers held), the mass term is formed as soon as u_prev arrives
+  {
+    double uc[kEll];
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) uc[k] = P.u[vo + static_cast<size_t>(c[k]) * kLanes];
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) us[k][lane] = uc[k];
+  }
+  const double* me = P.ME + static_cast<size_t>(i) * kEll;
+  double mr = 0.0;
+  if (!first) {
+    double upc[kEll];
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) upc[k] = P.uprev[vo + static_cast<size_t>(c[k]) * kLanes];
+    // mass term M (u - u_prev)/dt, zero at the first Newton iterate of a step
+#pragma unroll
+    for (int k = 0; k < kEll; ++k)
+      if (k < len) mr += __ldg(me + k) * ((us[k][lane] - upc[k]) / P.dt);
+  }
+  double ku = 0.0;
+  if (shared_row) {
+    const double* ke = P.KE + static_cast<size_t>(i) * kEll;
+#pragma unroll
+    for (int k = 0; k < kEll; ++k)
+      if (k < len) ku += __ldg(ke + k) * us[k][lane];
+    refill_finish(P, i, sys, vo, step, first, true, ku, mr, 0.0, acc);
+    return;
+  }
+  double jv[kEll];
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) jv[k] = 0.0;
+  if constexpr (NPE > 0) {
+    // each lane reads back only its own scratch column: no warp sync (lanes of
+    // a warp may be in different actions)
+    const int q0 = __ldg(P.adj_ptr + i), q1 = __ldg(P.adj_ptr + i + 1);
+    for (int q = q0; q < q1; ++q) {
+      const int2 ea = __ldg(P.adj + q);
+      const int e = ea.x;
+      int rel[NPE];
+      Elem<NPE> E;
+#pragma unroll
+      for (int b = 0; b < NPE; ++b) {
+        rel[b] = __ldg(P.adj_rel + static_cast<size_t>(q) * NPE + b);
+        E.ue[b] = rel[b] >= 0 ? us[rel[b]][lane] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < NPE * NPE; ++k) E.S[k] = __ldg(P.eS + static_cast<size_t>(e) * NPE * NPE + k);
+      double b2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < NPE; ++a) {
+        double sg = 0.0;
+#pragma unroll
+        for (int b = 0; b < NPE; ++b) sg += E.S[a * NPE + b] * E.ue[b];
+        E.g[a] = sg;
+        b2 += E.ue[a] * sg;
+      }
+      const double inva = __ldg(P.einvA + e);
+      b2 *= inva;
+      double nup;
+      curve_eval(curves[__ldg(P.ecurve + e)], b2, E.nu, nup);
+      E.cc = 2.0 * nup * inva;
+      double ga, Sa[NPE];
+      elem_row<NPE>(E, ea.y, ga, Sa);
+      ku += E.nu * ga;
+#pragma unroll
+      for (int b = 0; b < NPE; ++b) {
+        if (rel[b] < 0) continue;
+        const double v = E.nu * Sa[b] + E.cc * (ga * E.g[b]);
+#pragma unroll
+        for (int sl = 0; sl < kEll; ++sl) jv[sl] += (rel[b] == sl) ? v : 0.0;
+      }
+    }
+  }
+  double dval = 0.0;
+  const int dslot = __ldg(P.diag + i) - base;
+  double* Arow = P.A + ao + static_cast<size_t>(base) * kLanes;
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) {
+    if (k >= len) break;
+    const double av = __ldg(me + k) / P.dt + jv[k];
+    Arow[k * kLanes] = av;
+    if (k == dslot) dval = av;
+  }
+  refill_finish(P, i, sys, vo, step, first, false, ku, mr, dval, acc);
 }
 
 // Row epilogue of the refill: excitation, residual R = M(u - u_prev)/dt + K(u)u
@@ -672,7 +774,11 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     if (lane == 0) any_a = 0, any_r = !LINEAR;
   }
   __syncthreads();
-  extern __shared__ __align__(16) int4 srec[];
+  // dynamic shared memory: the refill slot scratch (a row's u entries per
+  // warp), then the block's row records
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  double(*uscr)[kEll][32] = reinterpret_cast<double(*)[kEll][32]>(dyn_smem);
+  int4* srec = reinterpret_cast<int4*>(dyn_smem + kScrSmem);
   stage_records(P, c, srec);
   const bool writer = (c == 0) && (warp == 0) && valid;
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
@@ -697,7 +803,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     const int act = lact[sl];
     const int step = lstep[sl];
     if (P.dbg && threadIdx.x == 0) t_start = globaltimer_ns();
-    const int dbg_kind = act == ACT_A ? 0 : (act == ACT_B ? 1 : 2);
+    const int dbg_kind = any_r ? 2 : (any_a ? 0 : 1);  // refill in the interval, else phase A, else the rest
     double* xs = LINEAR ? ((step & 1) ? P.ubuf0 : P.ubuf1) : P.x;
     // per-interval addressing from opaque copies of (g, c, warp, lane): the
     // compiler cannot hoist it and keep it live across the whole loop
@@ -727,9 +833,13 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         update_range<LINEAR>(P, rec, xs, S, vo, lanes[sl].alpha, lanes[sl].beta, lanes[sl].pit == 0, acc);
     } else if (act == ACT_R0 || act == ACT_R) {
       if (!LINEAR)
-        for (int i = row_begin; i < row_end; i += row_step) {
-          if (P.n_long > 0 && __ldg(P.rp + i + 1) - __ldg(P.rp + i) > kLongRow) continue;  // refill_long_rows
-          refill_row<NPE>(P, sh_curves, i, sys, vo, ao, step, act == ACT_R0, acc);
+        for (int i = row_begin, ri = S.ri0; i < row_end; i += row_step, ri += S.rstep) {
+          const int len = rec[kRecInts4 * ri].y;
+          if (len <= kEll)
+            refill_row_ell<NPE>(P, sh_curves, rec, ri, i, sys, vo, ao, step, act == ACT_R0, uscr[wq], acc);
+          else if (len <= kLongRow)
+            refill_row<NPE>(P, sh_curves, i, sys, vo, ao, step, act == ACT_R0, acc);
+          // longer rows: refill_long_rows
         }
     } else if (act == ACT_U) {
       if (!lanes[sl].zero_dx) {
@@ -967,8 +1077,8 @@ __global__ void __launch_bounds__(kThreads, 1) phase_probe_kernel(const PropPara
   const int g = blockIdx.x / P.C, c = blockIdx.x % P.C;
   const size_t vo = static_cast<size_t>(g) * P.d * kLanes + lane;
   const size_t ao = static_cast<size_t>(g) * P.nnz * kLanes + lane;
-  extern __shared__ __align__(16) int4 srec[];
-  const int4* rec = stage_records(P, c, srec);
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  const int4* rec = stage_records(P, c, reinterpret_cast<int4*>(dyn_smem + kScrSmem));
   const RowSeq S = warp_rows(P, c, warp);
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
   if (mode == 1)
@@ -1115,7 +1225,7 @@ int max_coresident_blocks(bool linear, int npe, int* out) {
   int best = 1 << 30;
   void* fns[] = {kernel_ptr<true, 0>(), kernel_ptr<false, 0>(), kernel_ptr<false, 2>(), kernel_ptr<false, 3>()};
   for (int k = 0; k < 4; ++k) {
-    const size_t smem = kRecSmemMax;
+    const size_t smem = kScrSmem + kRecSmemMax;
     if (smem &&
         cudaFuncSetAttribute(fns[k], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
             cudaSuccess)
@@ -1133,7 +1243,7 @@ int launch_propagate(const PropParams& prm, bool linear, int npe, cudaStream_t s
   void* fn = select_kernel(linear, npe);
   PropParams local = prm;
   void* args[] = {&local};
-  const size_t smem = static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4);
+  const size_t smem = kScrSmem + static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4);
   const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(prm.G * prm.C), dim3(kThreads), args, smem, st);
   if (e != cudaSuccess) {
     if (err) *err = std::string("cuda: propagate launch failed: ") + cudaGetErrorString(e);
@@ -1227,7 +1337,7 @@ void launch_eval_curve(const ps_curve& c, int n, const double* b2, double* nu, d
 }
 
 int launch_phase_probe(const PropParams& prm, int mode, double* sink, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4);
+  const size_t smem = kScrSmem + static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4);
   if (cudaFuncSetAttribute(reinterpret_cast<const void*>(phase_probe_kernel),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
     return PS_ERR_CUDA;

@@ -26,7 +26,8 @@ constexpr int kLongRow = 32;           // rows with > 32 slots are split across 
 // persistent kernels copy their block's records into shared memory once.
 constexpr int kEll = 8;
 constexpr int kRecInts4 = 3;                          // int4 per row record
-constexpr size_t kRecSmemMax = 176 * 1024;            // dynamic shared memory for records
+constexpr size_t kScrSmem = static_cast<size_t>(kWarps) * kEll * 32 * sizeof(double);  // refill slot scratch
+constexpr size_t kRecSmemMax = 144 * 1024;            // dynamic shared memory for records (after the scratch)
 
 // Per-system outcome written by block 0 of every group.
 struct SysOut {
@@ -57,6 +58,8 @@ struct PropParams {
   const int* diag;
   const int4* rowrec;   // [d][kRecInts4]
   int rec_rows;          // >0: largest block row range; records are staged in shared memory
+  const double* ME;      // [d][kEll] padded mass rows
+  const double* KE;      // [d][kEll] padded shared stiffness rows (K linear, K_const element problems)
   int chunk_rot;         // chunk k of kWarps rows belongs to block (k + chunk_rot) mod C
   int pf_dist;           // phase-A L2 prefetch distance in rows; 0 = off
   int hub_split;         // 1: the single long row's phase-A product goes through the reduction
@@ -125,6 +128,8 @@ struct DevProblem {
   int* ci = nullptr;
   int* diag = nullptr;
   int4* rowrec = nullptr;
+  double* ME = nullptr;  // [d][kEll] padded mass rows
+  double* KE = nullptr;  // [d][kEll] padded shared stiffness rows (K or K_const)
   double* M = nullptr;
   double* K = nullptr;        // linear K (or frozen K-bar)
   int* adj_ptr = nullptr;
