@@ -260,7 +260,10 @@ def run_ours(args):
             ev1.record(stream)
         barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
-    launches = 3 * args.steps  # transpose in, persistent propagation kernel, transpose out
+    # per step: one blocked-layout transpose per 32-system group in, the
+    # persistent propagation kernel, one transpose per group out
+    groups = (N + 31) // 32
+    launches = (2 * groups + 1) * args.steps
 
     # e2e: the public host-array API, H2D of the start states and D2H of F inside
     barrier()
