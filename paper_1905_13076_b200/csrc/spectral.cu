@@ -49,6 +49,9 @@ struct CocgParams {
   const int* diag;
   const double* X;  // Q (or K)
   const double* Y;  // C = M/dT (or M)
+  const int4* rowrec;   // [d][3] row records (pppc_internal.h): {base, len, kind, 0}, padded columns
+  const double2* XYE;   // [d][kEll] padded (X, Y) slot values of rows with <= kEll slots
+  const double2* dXY;   // [d] (X, Y) at the diagonal slot
   const double2* shift;  // [H] Lambda_b = X + shift_b * Y
   const double2* b;      // rhs_hat [d][H]
   double2* x;
@@ -73,9 +76,43 @@ struct BinLane {
 };
 
 __device__ __forceinline__ double2 lam_diag(const CocgParams& P, int i, double2 s) {
-  const int k = __ldg(P.diag + i);
-  const double xv = __ldg(P.X + k), yv = __ldg(P.Y + k);
-  return make_double2(xv + s.x * yv, s.y * yv);
+  const double2 xy = __ldg(P.dXY + i);
+  return make_double2(xy.x + s.x * xy.y, s.y * xy.y);
+}
+
+__device__ __forceinline__ double2 jacobi(double2 xy, double2 s) {
+  return cdiv(make_double2(1.0, 0.0), make_double2(xy.x + s.x * xy.y, s.y * xy.y));
+}
+
+// Phase A for one row of <= kEll slots: every load of the row (padded slot
+// values, the eight gathered p entries, own p, r and the diagonal) is issued
+// before the first FMA; the row record came one row earlier.  Pad slots carry
+// (X, Y) = 0 and point at the row itself.
+__device__ __forceinline__ void cocg_row_a(const CocgParams& P, int i, const int4& c03, const int4& c47, size_t H,
+                                           int h, double2 s_b, double (&acc)[kCND]) {
+  const int c[kEll] = {c03.x, c03.y, c03.z, c03.w, c47.x, c47.y, c47.z, c47.w};
+  double2 xy[kEll], pv[kEll];
+  const double2* xr = P.XYE + static_cast<size_t>(i) * kEll;
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) xy[k] = __ldg(xr + k);
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) pv[k] = P.p[static_cast<size_t>(c[k]) * H + h];
+  const size_t iv = static_cast<size_t>(i) * H + h;
+  const double2 pi = P.p[iv], ri = P.r[iv];
+  const double2 dxy = __ldg(P.dXY + i);
+  double2 qv = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) qv = cadd(qv, cmul(make_double2(xy[k].x + s_b.x * xy[k].y, s_b.y * xy[k].y), pv[k]));
+  P.q[iv] = qv;
+  const double2 dinv = jacobi(dxy, s_b);
+  const double2 zi = cmul(dinv, ri);
+  const double2 pq = cmul(pi, qv), qz = cmul(qv, zi), qdq = cmul(qv, cmul(dinv, qv));
+  acc[0] += pq.x;
+  acc[1] += pq.y;
+  acc[2] += qz.x;
+  acc[3] += qz.y;
+  acc[4] += qdq.x;
+  acc[5] += qdq.y;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
@@ -166,51 +203,51 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
       }
       __syncthreads();
     }
-    if (s.act)
-      for (int i = row_begin + sub; i < row_end; i += P.R) {
-        const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
-        const int len = end - base;
-        if (len > kLongRow) continue;
-        double2 qv = make_double2(0.0, 0.0);
-        if (len <= 8) {
-          // issue every index / value / gathered-operand load before the first FMA
-          int cj[8];
-          double xv[8], yv[8];
-          double2 pv[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) cj[k] = k < len ? __ldg(P.ci + base + k) : i;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            xv[k] = k < len ? __ldg(P.X + base + k) : 0.0;
-            yv[k] = k < len ? __ldg(P.Y + base + k) : 0.0;
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            pv[k] = k < len ? P.p[static_cast<size_t>(cj[k]) * H + h] : make_double2(0.0, 0.0);
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (k < len) qv = cadd(qv, cmul(make_double2(xv[k] + s_b.x * yv[k], s_b.y * yv[k]), pv[k]));
-        } else {
-          for (int k = base; k < end; ++k) {
+    if (s.act && row_begin + sub < row_end) {
+      // row records one row ahead of their use
+      int i = row_begin + sub;
+      int4 h0 = __ldg(P.rowrec + kRecInts4 * i), c03 = __ldg(P.rowrec + kRecInts4 * i + 1),
+           c47 = __ldg(P.rowrec + kRecInts4 * i + 2);
+      for (;;) {
+        const int i1 = i + P.R;
+        const bool more = i1 < row_end;
+        int4 h1 = h0, d03 = c03, d47 = c47;
+        if (more) {
+          h1 = __ldg(P.rowrec + kRecInts4 * i1);
+          d03 = __ldg(P.rowrec + kRecInts4 * i1 + 1);
+          d47 = __ldg(P.rowrec + kRecInts4 * i1 + 2);
+        }
+        const int len = h0.y;
+        if (len <= kEll) {
+          cocg_row_a(P, i, c03, c47, H, h, s_b, acc);
+        } else if (len <= kLongRow) {
+          double2 qv = make_double2(0.0, 0.0);
+          for (int k = h0.x; k < h0.x + len; ++k) {
             const int j = __ldg(P.ci + k);
             const double xk = __ldg(P.X + k), yk = __ldg(P.Y + k);
             const double2 lam = make_double2(xk + s_b.x * yk, s_b.y * yk);
             qv = cadd(qv, cmul(lam, P.p[static_cast<size_t>(j) * H + h]));
           }
+          const size_t iv = static_cast<size_t>(i) * H + h;
+          P.q[iv] = qv;
+          const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
+          const double2 pi = P.p[iv], ri = P.r[iv];
+          const double2 zi = cmul(dinv, ri);
+          const double2 pq = cmul(pi, qv), qz = cmul(qv, zi), qdq = cmul(qv, cmul(dinv, qv));
+          acc[0] += pq.x;
+          acc[1] += pq.y;
+          acc[2] += qz.x;
+          acc[3] += qz.y;
+          acc[4] += qdq.x;
+          acc[5] += qdq.y;
         }
-        const size_t iv = static_cast<size_t>(i) * H + h;
-        P.q[iv] = qv;
-        const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
-        const double2 pi = P.p[iv], ri = P.r[iv];
-        const double2 zi = cmul(dinv, ri);
-        const double2 pq = cmul(pi, qv), qz = cmul(qv, zi), qdq = cmul(qv, cmul(dinv, qv));
-        acc[0] += pq.x;
-        acc[1] += pq.y;
-        acc[2] += qz.x;
-        acc[3] += qz.y;
-        acc[4] += qdq.x;
-        acc[5] += qdq.y;
+        if (!more) break;
+        i = i1;
+        h0 = h1;
+        c03 = d03;
+        c47 = d47;
       }
+    }
     if (!group_sync_reduce<kCND, 6>(X, sh, acc, g, c)) return;
     ++lockstep;
     if (s.act) {
@@ -230,20 +267,35 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
       }
     }
     if (s.act)
-      for (int i = row_begin + sub; i < row_end; i += P.R) {
-        const size_t iv = static_cast<size_t>(i) * H + h;
-        const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
-        const double2 pi = P.p[iv], qi = P.q[iv];
-        double2 ri = P.r[iv];
-        P.x[iv] = cadd(P.x[iv], cmul(s.alpha, pi));
-        ri = csub(ri, cmul(s.alpha, qi));
-        const double2 zi = cmul(dinv, ri);
-        P.r[iv] = ri;
-        P.p[iv] = cadd(zi, cmul(s.beta, pi));
-        const double2 rz = cmul(ri, zi);
-        acc[0] += ri.x * ri.x + ri.y * ri.y;
-        acc[1] += rz.x;
-        acc[2] += rz.y;
+      // rows in pairs whose loads are issued together
+      for (int i0 = row_begin + sub; i0 < row_end; i0 += 2 * P.R) {
+        double2 xv[2], pv[2], qv[2], rv[2], dxy[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = i0 + u * P.R < row_end ? i0 + u * P.R : i0;
+          const size_t iv = static_cast<size_t>(i) * H + h;
+          dxy[u] = __ldg(P.dXY + i);
+          xv[u] = P.x[iv];
+          pv[u] = P.p[iv];
+          qv[u] = P.q[iv];
+          rv[u] = P.r[iv];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = i0 + u * P.R;
+          if (i >= row_end) break;
+          const size_t iv = static_cast<size_t>(i) * H + h;
+          const double2 dinv = jacobi(dxy[u], s_b);
+          P.x[iv] = cadd(xv[u], cmul(s.alpha, pv[u]));
+          const double2 ri = csub(rv[u], cmul(s.alpha, qv[u]));
+          const double2 zi = cmul(dinv, ri);
+          P.r[iv] = ri;
+          P.p[iv] = cadd(zi, cmul(s.beta, pv[u]));
+          const double2 rz = cmul(ri, zi);
+          acc[0] += ri.x * ri.x + ri.y * ri.y;
+          acc[1] += rz.x;
+          acc[2] += rz.y;
+        }
       }
     if (!group_sync_reduce<kCND, 3>(X, sh, acc, g, c)) return;
     if (s.act) {
@@ -499,6 +551,8 @@ struct SpectralState {
   double* X = nullptr;
   double* Y = nullptr;
   double* Q = nullptr;  // C + K for the RHS
+  double2* XYE = nullptr;  // [d][kEll] padded (X, Y) slot values
+  double2* dXY = nullptr;  // [d] diagonal (X, Y)
   double2* shift = nullptr;
   double2* tw = nullptr;
   int* d_bins = nullptr;
@@ -593,6 +647,25 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
     cudaMemcpy(s->Y, p.h_M.data(), p.nnz * sizeof(double), cudaMemcpyHostToDevice);
   }
   cudaMemcpy(s->Q, hQ.data(), p.nnz * sizeof(double), cudaMemcpyHostToDevice);
+  {
+    // padded (X, Y) rows and diagonal pairs for the COCG SpMV / Jacobi
+    const std::vector<double>& hX = shift_kind == 0 ? hQ : p.h_K;
+    const std::vector<double>& hY = shift_kind == 0 ? hC : p.h_M;
+    std::vector<double2> xye(static_cast<size_t>(p.d) * kEll, make_double2(0.0, 0.0)), dxy(p.d);
+    for (int i = 0; i < p.d; ++i) {
+      const int b = p.h_rp[i], len = p.h_rp[i + 1] - b;
+      if (len <= kEll)
+        for (int k = 0; k < len; ++k) xye[static_cast<size_t>(i) * kEll + k] = make_double2(hX[b + k], hY[b + k]);
+      const int dk = p.h_diag[i];
+      dxy[i] = make_double2(hX[dk], hY[dk]);
+    }
+    rc |= dalloc(&s->XYE, xye.size());
+    rc |= dalloc(&s->dXY, dxy.size());
+    if (rc == PS_OK) {
+      cudaMemcpy(s->XYE, xye.data(), xye.size() * sizeof(double2), cudaMemcpyHostToDevice);
+      cudaMemcpy(s->dXY, dxy.data(), dxy.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    }
+  }
   cudaMemcpy(s->shift, hs.data(), hs.size() * sizeof(double2), cudaMemcpyHostToDevice);
   const auto tw = twiddles(N);
   cudaMemcpy(s->tw, tw.data(), N * sizeof(double2), cudaMemcpyHostToDevice);
@@ -668,7 +741,7 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
 
 void spectral_free(SpectralState* s) {
   if (!s) return;
-  void* ptrs[] = {s->warp_row_begin, s->long_rows, s->long_owner, s->X, s->Y, s->Q, s->shift, s->tw, s->d_bins, s->rhs, s->bhat,
+  void* ptrs[] = {s->XYE, s->dXY, s->warp_row_begin, s->long_rows, s->long_owner, s->X, s->Y, s->Q, s->shift, s->tw, s->d_bins, s->rhs, s->bhat,
                   s->x, s->r, s->p, s->q, s->sync, s->partials, s->abort_flag, s->code, s->iters,
                   s->lockstep, s->jpart, s->maxre, s->maxim, s->jout, s->coef};
   for (void* ptr : ptrs)
@@ -717,6 +790,9 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
     P.diag = p.diag;
     P.X = s->X;
     P.Y = s->Y;
+    P.rowrec = p.rowrec;
+    P.XYE = s->XYE;
+    P.dXY = s->dXY;
     P.shift = s->shift;
     P.b = s->bhat;
     P.x = s->x;
