@@ -339,47 +339,85 @@ __global__ void assemble_rhs_kernel(int d, int N, const int* __restrict__ rp, co
   rhs[t] = acc + f;
 }
 
+// Spectral tiles: a block stages kDftRows consecutive DOFs' samples (or
+// spectra) and the twiddle table in shared memory with coalesced loads, then
+// every thread owns output slots of the tile.  Blocks stride over tiles.
+constexpr int kDftRows = 8;
+
 // rhs_hat[i][h] = N^{-1/2} sum_n rhs[i][n] exp(-2 pi i bin_h n / N)
+// (proj/src/spectral.cpp:32-63; the same n order and incremental twiddle index
+// as a per-DOF loop).  Thread slot = (row of the tile, bin): consecutive
+// threads write consecutive out entries.
 __global__ void dft_forward_kernel(int d, int N, int H, const int* __restrict__ bins, const double2* __restrict__ tw,
-                                   const double* rhs, double2* out) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= static_cast<int64_t>(d) * H) return;
-  const int hh = static_cast<int>(t % H), i = static_cast<int>(t / H);
-  const int b = bins[hh];
-  const double* row = rhs + static_cast<size_t>(i) * N;
-  double ar = 0.0, ai = 0.0;
-  int idx = 0;
-  for (int n = 0; n < N; ++n) {
-    const double v = row[n];
-    const double2 w = tw[idx];
-    ar += v * w.x;
-    ai += v * w.y;
-    idx += b;
-    if (idx >= N) idx -= N;
-  }
+                                   const double* __restrict__ rhs, double2* __restrict__ out) {
+  extern __shared__ double2 dsm[];
+  double2* stw = dsm;                                              // [N]
+  double* srow = reinterpret_cast<double*>(dsm + N);               // [kDftRows][N]
+  int* sbin = reinterpret_cast<int*>(srow + kDftRows * N);         // [H]
+  for (int k = threadIdx.x; k < N; k += blockDim.x) stw[k] = tw[k];
+  for (int k = threadIdx.x; k < H; k += blockDim.x) sbin[k] = bins[k];
   const double scale = 1.0 / sqrt(static_cast<double>(N));
-  out[t] = make_double2(scale * ar, scale * ai);
+  const int tiles = (d + kDftRows - 1) / kDftRows;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int i0 = tile * kDftRows;
+    const int rows = min(kDftRows, d - i0);
+    __syncthreads();
+    const double* src = rhs + static_cast<size_t>(i0) * N;
+    for (int k = threadIdx.x; k < rows * N; k += blockDim.x) srow[k] = src[k];
+    __syncthreads();
+    for (int slot = threadIdx.x; slot < rows * H; slot += blockDim.x) {
+      const int r = slot / H, hh = slot - r * H;
+      const int b = sbin[hh];
+      const double* row = srow + r * N;
+      double ar = 0.0, ai = 0.0;
+      int idx = 0;
+      for (int n = 0; n < N; ++n) {
+        const double v = row[n];
+        const double2 w = stw[idx];
+        ar += v * w.x;
+        ai += v * w.y;
+        idx += b;
+        if (idx >= N) idx -= N;
+      }
+      out[static_cast<size_t>(i0) * H + slot] = make_double2(scale * ar, scale * ai);
+    }
+  }
 }
 
-// U_new[i][n] = N^{-1/2} sum over the (mirrored) spectrum, realified; fused with
-// the jump partials (per-block, per-n sums of |U_new - U_old|^2 and |U_new|^2)
-// and the max |re| / max |im| of the realify check.
+// U_new[i][n] = N^{-1/2} sum over the (mirrored) spectrum, realified
+// (proj/src/spectral.cpp:72-84,270-278); fused with the jump partials
+// (proj/src/engine.cpp:54-64: per-n sums of |U_new - U_old|^2 and |U_new|^2)
+// and the max |re| / max |im| of the realify check.  blockDim = k * N: thread t
+// owns sample n = t mod N for rows t / N, t / N + k, ... of every tile it
+// visits, so its partial sums run in a fixed order; part[block][2][N].
 __global__ void idft_jump_kernel(int d, int N, int H, const int* __restrict__ bins, const double2* __restrict__ tw,
-                                 int conj, const double2* xhat, double* U, const double* U_old, double* part,
-                                 double* maxre, double* maxim) {
-  extern __shared__ double smem[];  // [2][nwarps][N]
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+                                 int conj, const double2* __restrict__ xhat, double* __restrict__ U,
+                                 const double* __restrict__ U_old, double* part, double* maxre, double* maxim) {
+  extern __shared__ double2 ism[];
+  double2* stw = ism;                                         // [N]
+  double2* sx = ism + N;                                      // [kDftRows][H]
+  double* sred = reinterpret_cast<double*>(sx + kDftRows * H);  // [blockDim] x 2
+  int* sbin = reinterpret_cast<int*>(sred + 2 * blockDim.x);  // [H]
+  for (int k = threadIdx.x; k < N; k += blockDim.x) stw[k] = tw[k];
+  for (int k = threadIdx.x; k < H; k += blockDim.x) sbin[k] = bins[k];
+  const int n = threadIdx.x % N, r0 = threadIdx.x / N, kr = blockDim.x / N;
   const double scale = 1.0 / sqrt(static_cast<double>(N));
-  double mre = 0.0, mim = 0.0;
-  for (int n = 0; n < N; ++n) {
-    double vr = 0.0, vi = 0.0;
-    if (i < d) {
+  double dd = 0.0, nn = 0.0, mre = 0.0, mim = 0.0;
+  const int tiles = (d + kDftRows - 1) / kDftRows;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int i0 = tile * kDftRows;
+    const int rows = min(kDftRows, d - i0);
+    __syncthreads();
+    const double2* src = xhat + static_cast<size_t>(i0) * H;
+    for (int k = threadIdx.x; k < rows * H; k += blockDim.x) sx[k] = src[k];
+    __syncthreads();
+    for (int r = r0; r < rows; r += kr) {
+      const double2* xr = sx + r * H;
+      double vr = 0.0, vi = 0.0;
       for (int hh = 0; hh < H; ++hh) {
-        const int b = bins[hh];
-        const double2 xv = xhat[static_cast<size_t>(i) * H + hh];
-        const double2 w = tw[(static_cast<int64_t>(b) * n) % N];  // exp(-2 pi i b n/N); inverse uses conj
-        // xv * conj(w)
+        const int b = sbin[hh];
+        const double2 xv = xr[hh];
+        const double2 w = stw[(b * n) % N];  // exp(-2 pi i b n/N), b n < 2^20; inverse uses conj
         const double cr = xv.x * w.x + xv.y * w.y;
         const double cim = xv.y * w.x - xv.x * w.y;
         if (conj && b != 0 && 2 * b != N) {
@@ -393,59 +431,84 @@ __global__ void idft_jump_kernel(int d, int N, int H, const int* __restrict__ bi
       vi *= scale;
       mre = fmax(mre, fabs(vr));
       mim = fmax(mim, fabs(vi));
-    }
-    double dd = 0.0, nn = 0.0;
-    if (i < d) {
-      const size_t iv = static_cast<size_t>(i) * N + n;
+      const size_t iv = static_cast<size_t>(i0 + r) * N + n;
       if (U_old) {
         const double df = vr - U_old[iv];
-        dd = df * df;
+        dd += df * df;
       }
-      nn = vr * vr;
+      nn += vr * vr;
       U[iv] = vr;
     }
-    for (int off = 16; off > 0; off >>= 1) {
-      dd += __shfl_xor_sync(0xffffffffu, dd, off);
-      nn += __shfl_xor_sync(0xffffffffu, nn, off);
-    }
-    if (lane == 0) {
-      smem[(0 * nw + warp) * N + n] = dd;
-      smem[(1 * nw + warp) * N + n] = nn;
-    }
   }
-  for (int off = 16; off > 0; off >>= 1) {
-    mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, off));
-    mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, off));
+  // per-n partials: the kr threads of sample n combine in row order
+  __syncthreads();
+  sred[threadIdx.x] = dd;
+  sred[blockDim.x + threadIdx.x] = nn;
+  __syncthreads();
+  for (int m = threadIdx.x; m < N; m += blockDim.x) {
+    double a = 0.0, b2 = 0.0;
+    for (int k = 0; k < kr; ++k) {
+      a += sred[k * N + m];
+      b2 += sred[blockDim.x + k * N + m];
+    }
+    part[(static_cast<size_t>(blockIdx.x) * 2 + 0) * N + m] = a;
+    part[(static_cast<size_t>(blockIdx.x) * 2 + 1) * N + m] = b2;
   }
   __syncthreads();
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+  sred[threadIdx.x] = mre;
+  sred[blockDim.x + threadIdx.x] = mim;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     double a = 0.0, b2 = 0.0;
-    for (int w = 0; w < nw; ++w) {
-      a += smem[(0 * nw + w) * N + n];
-      b2 += smem[(1 * nw + w) * N + n];
+    for (int k = 0; k < static_cast<int>(blockDim.x); ++k) {
+      a = fmax(a, sred[k]);
+      b2 = fmax(b2, sred[blockDim.x + k]);
     }
-    part[(static_cast<size_t>(blockIdx.x) * 2 + 0) * N + n] = a;
-    part[(static_cast<size_t>(blockIdx.x) * 2 + 1) * N + n] = b2;
-  }
-  if (lane == 0) {
-    maxre[blockIdx.x * nw + warp] = mre;
-    maxim[blockIdx.x * nw + warp] = mim;
+    maxre[blockIdx.x] = a;
+    maxim[blockIdx.x] = b2;
   }
 }
 
 // out[0] = jump, out[1] = max_n |dU_n|, out[2] = max_n |U_n|, out[3] = max|re|, out[4] = max|im|
+// One block of 1024 threads: thread (n, j) sums the block partials j, j + 4,
+// ... of sample n (eight loads in flight), the four sub-sums combine in order.
 __global__ void jump_finalize_kernel(int N, int nblocks, int nmax, const double* part, const double* maxre,
                                      const double* maxim, double* out) {
-  __shared__ double sd[1024], sn[1024], sr[1024], si[1024];
+  constexpr int kSub = 4;
+  __shared__ double sa[1024], sb[1024], sd[1024], sn[1024], sr[1024], si[1024];
+  const int j = threadIdx.x % kSub, t = threadIdx.x / kSub, nt = blockDim.x / kSub;
   double bd = 0.0, bn = 0.0;
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+  for (int n0 = 0; n0 < N; n0 += nt) {
+    const int n = n0 + t;
     double a = 0.0, b = 0.0;
-    for (int k = 0; k < nblocks; ++k) {
-      a += part[(static_cast<size_t>(k) * 2 + 0) * N + n];
-      b += part[(static_cast<size_t>(k) * 2 + 1) * N + n];
+    if (n < N)
+      for (int k0 = j; k0 < nblocks; k0 += 8 * kSub) {
+        double va[8], vb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = k0 + u * kSub;
+          va[u] = k < nblocks ? part[(static_cast<size_t>(k) * 2 + 0) * N + n] : 0.0;
+          vb[u] = k < nblocks ? part[(static_cast<size_t>(k) * 2 + 1) * N + n] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a += va[u];
+          b += vb[u];
+        }
+      }
+    sa[threadIdx.x] = a;
+    sb[threadIdx.x] = b;
+    __syncthreads();
+    if (j == 0 && n < N) {
+      double A = 0.0, B = 0.0;
+      for (int q = 0; q < kSub; ++q) {
+        A += sa[threadIdx.x + q];
+        B += sb[threadIdx.x + q];
+      }
+      bd = fmax(bd, sqrt(A));
+      bn = fmax(bn, sqrt(B));
     }
-    bd = fmax(bd, sqrt(a));
-    bn = fmax(bn, sqrt(b));
+    __syncthreads();
   }
   double mr = 0.0, mi = 0.0;
   for (int k = threadIdx.x; k < nmax; k += blockDim.x) {
@@ -457,19 +520,21 @@ __global__ void jump_finalize_kernel(int N, int nblocks, int nmax, const double*
   sr[threadIdx.x] = mr;
   si[threadIdx.x] = mi;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double D = 0.0, Nn = 0.0, R = 0.0, I = 0.0;
-    for (int k = 0; k < blockDim.x; ++k) {
-      D = fmax(D, sd[k]);
-      Nn = fmax(Nn, sn[k]);
-      R = fmax(R, sr[k]);
-      I = fmax(I, si[k]);
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (static_cast<int>(threadIdx.x) < w) {
+      sd[threadIdx.x] = fmax(sd[threadIdx.x], sd[threadIdx.x + w]);
+      sn[threadIdx.x] = fmax(sn[threadIdx.x], sn[threadIdx.x + w]);
+      sr[threadIdx.x] = fmax(sr[threadIdx.x], sr[threadIdx.x + w]);
+      si[threadIdx.x] = fmax(si[threadIdx.x], si[threadIdx.x + w]);
     }
-    out[0] = D / fmax(1.0, Nn);
-    out[1] = D;
-    out[2] = Nn;
-    out[3] = R;
-    out[4] = I;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = sd[0] / fmax(1.0, sn[0]);
+    out[1] = sd[0];
+    out[2] = sn[0];
+    out[3] = sr[0];
+    out[4] = si[0];
   }
 }
 
@@ -588,6 +653,10 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
   if (!p.linear) {
     *err = "spectral: cyclic system requires a linear problem (freeze the coarse operator first)";
     return PS_ERR_NOT_LINEAR;
+  }
+  if (N > 1024) {
+    *err = "spectral: multiharmonic solve supports at most 1024 blocks, got " + std::to_string(N);
+    return PS_ERR_BAD_ARG;
   }
   auto* s = new SpectralState();
   s->N = N;
@@ -709,10 +778,16 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
     rc |= dalloc(&s->iters, s->H);
     rc |= dalloc(&s->lockstep, s->G);
   }
-  s->idft_blocks = (p.d + 127) / 128;
+  {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = (p.d + kDftRows - 1) / kDftRows;
+    s->idft_blocks = std::max(1, std::min(tiles, sms * 8));
+  }
   rc |= dalloc(&s->jpart, static_cast<size_t>(s->idft_blocks) * 2 * N);
-  rc |= dalloc(&s->maxre, static_cast<size_t>(s->idft_blocks) * 4);
-  rc |= dalloc(&s->maxim, static_cast<size_t>(s->idft_blocks) * 4);
+  rc |= dalloc(&s->maxre, static_cast<size_t>(s->idft_blocks));
+  rc |= dalloc(&s->maxim, static_cast<size_t>(s->idft_blocks));
   rc |= dalloc(&s->jout, 8);
   rc |= dalloc(&s->coef, static_cast<size_t>(N) * std::max(1, p.nterms));
   // excitation coefficients at T_sub for every row (assemble_rhs)
@@ -728,6 +803,11 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
     }
   }
   cudaMemcpy(s->coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice);
+  // spectral tiles: up to 1024 samples and 513 bins in dynamic shared memory
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(dft_forward_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       160 * 1024);
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(idft_jump_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       160 * 1024);
   cudaEventCreate(&s->e0);
   cudaEventCreate(&s->e1);
   if (rc != PS_OK || cudaGetLastError() != cudaSuccess) {
@@ -769,8 +849,11 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
   int max_its = 0;
   if (H > 0) {
     const int64_t tot = static_cast<int64_t>(d) * H;
-    dft_forward_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(d, N, H, s->d_bins, s->tw, rhs,
-                                                                                 s->bhat);
+    const size_t fsm = static_cast<size_t>(N) * sizeof(double2) + static_cast<size_t>(kDftRows) * N * sizeof(double) +
+                       static_cast<size_t>(H) * sizeof(int);
+    const int ftpb = std::min(1024, ((kDftRows * H + 31) / 32) * 32);
+    dft_forward_kernel<<<s->idft_blocks, ftpb, fsm, st>>>(d, N, H, s->d_bins, s->tw, rhs, s->bhat);
+    (void)tot;
     cudaMemsetAsync(s->sync, 0, s->G * sizeof(unsigned long long), st);
     cudaMemsetAsync(s->abort_flag, 0, sizeof(int), st);
     CocgParams P{};
@@ -815,12 +898,12 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
       return PS_ERR_CUDA;
     }
   }
-  const int tpb = 128;
-  const size_t smem = static_cast<size_t>(2) * (tpb / 32) * N * sizeof(double);
+  const int tpb = N * std::max(1, 512 / N);  // thread t owns sample t mod N
+  const size_t smem = static_cast<size_t>(N) * sizeof(double2) + static_cast<size_t>(kDftRows) * H * sizeof(double2) +
+                      static_cast<size_t>(2) * tpb * sizeof(double) + static_cast<size_t>(H) * sizeof(int);
   idft_jump_kernel<<<s->idft_blocks, tpb, smem, st>>>(d, N, H, s->d_bins, s->tw, s->conj, s->x, U_il, U_prev_il,
                                                       s->jpart, s->maxre, s->maxim);
-  jump_finalize_kernel<<<1, 256, 0, st>>>(N, s->idft_blocks, s->idft_blocks * (tpb / 32), s->jpart, s->maxre,
-                                          s->maxim, s->jout);
+  jump_finalize_kernel<<<1, 1024, 0, st>>>(N, s->idft_blocks, s->idft_blocks, s->jpart, s->maxre, s->maxim, s->jout);
   cudaEventRecord(s->e1, st);
   double hj[5];
   cudaMemcpyAsync(hj, s->jout, sizeof(hj), cudaMemcpyDeviceToHost, st);
