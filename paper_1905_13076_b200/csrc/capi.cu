@@ -379,6 +379,14 @@ int chunk_rotation() {
   return rot < 0 ? 0 : rot;
 }
 
+// Sequential group launches: the groups of a batch run one after another, each
+// on every co-resident block (C from one group), and the PCG residual of a
+// block's rows stays in shared memory.  PPPC_SEQ=0/1 overrides the default.
+bool sequential_groups() {
+  static const int v = std::getenv("PPPC_SEQ") ? std::atoi(std::getenv("PPPC_SEQ")) : 0;
+  return v != 0;
+}
+
 Geometry& geometry(ps_ctx* ctx, int count) {
   auto it = ctx->geo.find(count);
   if (it != ctx->geo.end()) return it->second;
@@ -391,7 +399,7 @@ Geometry& geometry(ps_ctx* ctx, int count) {
   g.L = (count + g.G - 1) / g.G;
   g.Lp = 32;
   g.R = 1;
-  const int g_max = (ctx->max_batch + 31) / 32;
+  const int g_max = sequential_groups() ? 1 : (ctx->max_batch + 31) / 32;
   const int rows_min = kWarps * 4;
   if (g_max > ctx->capacity) throw Failure(PS_ERR_BAD_ARG, "propagator: batch too large for one cooperative launch");
   g.C = std::max(1, std::min(ctx->capacity / g_max, (ctx->P.d + rows_min - 1) / rows_min));
@@ -522,6 +530,7 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.ME = P.ME;
   K.KE = P.KE;
   K.chunk_rot = chunk_rotation();
+  K.g_base = 0;
   K.hub_split = (geo.n_long == 1 && std::getenv("PPPC_NO_HUB_SPLIT") == nullptr) ? 1 : 0;
   {
     // phase-A L2 prefetch distance in rows, PPPC_PF (default 0 = off: it helps
@@ -530,6 +539,11 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
     K.pf_dist = pf < 0 ? 0 : pf;
   }
   K.rec_rows = geo.max_block_rows * kRecInts4 * sizeof(int4) <= kRecSmemMax ? geo.max_block_rows : 0;
+  // residual rows in shared memory when records + residual fit the opted-in size
+  K.r_smem = (sequential_groups() && K.rec_rows > 0 &&
+              static_cast<size_t>(K.rec_rows) * (kRecInts4 * sizeof(int4) + 32 * sizeof(double)) <= kRecSmemMax)
+                 ? 1
+                 : 0;
   K.M = P.M;
   K.Klin = P.K;
   K.Kc = P.Kc;
@@ -582,6 +596,7 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.trace = want_trace ? ctx->trace : nullptr;
   K.lockstep = ctx->lockstep;
   ctx->last_params = K;
+  ctx->last_params.r_smem = 0;  // phase probes keep r in global memory
   ctx->has_last_params = !linear_path;
 
   const int npe = P.linear ? 0 : P.npe;
@@ -615,8 +630,21 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   }
   check(cudaEventRecord(ctx->e0, ctx->stream), "event");
   std::string err;
-  const int rc = launch_propagate(K, linear_path, npe, ctx->stream, &err);
-  if (rc != PS_OK) throw Failure(rc, err);
+  if (sequential_groups() && geo.G > 1) {
+    // one launch per group, each on all C blocks, own arrival counter
+    for (int gg = 0; gg < geo.G; ++gg) {
+      PropParams Kg = K;
+      Kg.G = 1;
+      Kg.g_base = gg;
+      Kg.sync = K.sync + gg;
+      if (K.dbg) Kg.dbg = K.dbg + static_cast<size_t>(gg) * geo.C * kDbgSlots;
+      const int rc = launch_propagate(Kg, linear_path, npe, ctx->stream, &err);
+      if (rc != PS_OK) throw Failure(rc, err);
+    }
+  } else {
+    const int rc = launch_propagate(K, linear_path, npe, ctx->stream, &err);
+    if (rc != PS_OK) throw Failure(rc, err);
+  }
   check(cudaEventRecord(ctx->e1, ctx->stream), "event");
   std::vector<unsigned long long> h_dbg;
   if (K.dbg) {

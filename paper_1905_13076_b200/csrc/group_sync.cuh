@@ -31,7 +31,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 
 template <int NDMAX>
 struct SyncShared {
-  static constexpr int S = kThreads / (NDMAX * 32);  // interleaved sub-sums per (dot, lane)
+  static constexpr int S = kThreads / (NDMAX * 16);  // interleaved sub-sums per (dot, lane pair)
   double wpart[kWarps][NDMAX][32];
   double red[S][NDMAX][32];
   double tot[NDMAX][32];
@@ -55,6 +55,7 @@ struct SyncCtx {
   double* partials;          // [2][G][C][NDMAX][32]
   int* abort_flag;
   int G, C, Lp;
+  int L;                     // lanes carrying a system (the rest are padding and are not reduced)
 };
 
 // acc: this thread's partial sums (lane = system, sub-rows combined here).
@@ -111,24 +112,33 @@ __device__ bool group_sync_reduce(const SyncCtx& X, SyncShared<NDMAX>& sh, doubl
   __syncthreads();
   if (sh.abort) return false;
   {
+    // thread = (sub-sum s, dot k, lane pair lp): 16-byte loads of two lanes,
+    // kRedIlp of them in flight, partials of block c = s, s + S, ... summed
+    // in increasing c (fixed order); at C = 148 two rounds of L2 latency
+    constexpr int kRedIlp = 10;
     const int t = threadIdx.x;
-    const int s = t / (NDMAX * 32);
-    const int k = (t / 32) % NDMAX;
-    const int l = t & 31;
-    if (s < S && k < ND) {
-      // issue 8 independent loads per batch before adding (fixed summation order)
-      double v = 0.0;
-      for (int c0 = s; c0 < X.C; c0 += 8 * S) {
-        double tmp[8];
+    const int s = t / (NDMAX * 16);
+    const int k = (t / 16) % NDMAX;
+    const int lp = t & 15;
+    if (s < S && k < ND && 2 * lp < X.L) {
+      double2 v = make_double2(0.0, 0.0);
+      for (int c0 = s; c0 < X.C; c0 += kRedIlp * S) {
+        double2 tmp[kRedIlp];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kRedIlp; ++u) {
           const int cc = c0 + u * S;
-          tmp[u] = cc < X.C ? part[static_cast<size_t>(cc) * (NDMAX * 32) + k * 32 + l] : 0.0;
+          tmp[u] = cc < X.C ? *reinterpret_cast<const double2*>(part + static_cast<size_t>(cc) * (NDMAX * 32) +
+                                                                k * 32 + 2 * lp)
+                            : make_double2(0.0, 0.0);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v += tmp[u];
+        for (int u = 0; u < kRedIlp; ++u) {
+          v.x += tmp[u].x;
+          v.y += tmp[u].y;
+        }
       }
-      sh.red[s][k][l] = v;
+      sh.red[s][k][2 * lp] = v.x;
+      sh.red[s][k][2 * lp + 1] = v.y;
     }
   }
   __syncthreads();

@@ -143,12 +143,12 @@ __device__ __forceinline__ bool row_shared(const PropParams& P, int i) {
 }
 
 __device__ __forceinline__ void refill_finish(const PropParams& P, int i, int sys, size_t vo, int step, bool first,
-                                              bool shared_row, double ku, double mr, double dval,
+                                              bool shared_row, double ku, double mr, double dval, double* rdst,
                                               double (&acc)[kNDots]);
 
 template <int NPE>
 __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* curves, int i, int sys, size_t vo,
-                                           size_t ao, int step, bool first, double (&acc)[kNDots]) {
+                                           size_t ao, int step, bool first, double* rdst, double (&acc)[kNDots]) {
   const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
   const int len = end - base;
   const bool regular = len <= kRegularRow;
@@ -211,7 +211,7 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
     P.A[ao + static_cast<size_t>(k) * kLanes] = av;
     if (k == dslot) dval = av;
   }
-  refill_finish(P, i, sys, vo, step, first, shared_row, ku, mr, dval, acc);
+  refill_finish(P, i, sys, vo, step, first, shared_row, ku, mr, dval, rdst, acc);
 }
 
 // refill_row for a row of <= kEll slots, driven by its record (pppc_internal.h):
@@ -223,7 +223,7 @@ __device__ __forceinline__ void refill_row(const PropParams& P, const ps_curve* 
 template <int NPE>
 __device__ __forceinline__ void refill_row_ell(const PropParams& P, const ps_curve* curves, const int4* rec, int ri,
                                                int i, int sys, size_t vo, size_t ao, int step, bool first,
-                                               double (*us)[32], double (&acc)[kNDots]) {
+                                               double (*us)[32], double* rdst, double (&acc)[kNDots]) {
   const int lane = threadIdx.x & 31;
   const int4 h = rec[kRecInts4 * ri];
   const int4 c03 = rec[kRecInts4 * ri + 1], c47 = rec[kRecInts4 * ri + 2];
@@ -256,7 +256,7 @@ __device__ __forceinline__ void refill_row_ell(const PropParams& P, const ps_cur
 #pragma unroll
     for (int k = 0; k < kEll; ++k)
       if (k < len) ku += __ldg(ke + k) * us[k][lane];
-    refill_finish(P, i, sys, vo, step, first, true, ku, mr, 0.0, acc);
+    refill_finish(P, i, sys, vo, step, first, true, ku, mr, 0.0, rdst, acc);
     return;
   }
   double jv[kEll];
@@ -314,13 +314,13 @@ __device__ __forceinline__ void refill_row_ell(const PropParams& P, const ps_cur
     Arow[k * kLanes] = av;
     if (k == dslot) dval = av;
   }
-  refill_finish(P, i, sys, vo, step, first, false, ku, mr, dval, acc);
+  refill_finish(P, i, sys, vo, step, first, false, ku, mr, dval, rdst, acc);
 }
 
 // Row epilogue of the refill: excitation, residual R = M(u - u_prev)/dt + K(u)u
 // - f, Jacobi diagonal, r = -R, p = Dinv r, and the row's dot partials.
 __device__ __forceinline__ void refill_finish(const PropParams& P, int i, int sys, size_t vo, int step, bool first,
-                                              bool shared_row, double ku, double mr, double dval,
+                                              bool shared_row, double ku, double mr, double dval, double* rdst,
                                               double (&acc)[kNDots]) {
   const size_t iv = vo + static_cast<size_t>(i) * kLanes;
   // excitation f_i = sum_t c_t(t_next) pattern_t[i]  (proj/src/problem.cpp:52-63)
@@ -332,7 +332,7 @@ __device__ __forceinline__ void refill_finish(const PropParams& P, int i, int sy
   const double r = -R;
   const double z = dinv * r;
   if (!shared_row) P.Dinv[iv] = dinv;
-  P.r[iv] = r;
+  *rdst = r;
   P.p[iv] = z;
   if (first) P.uprev[iv] = P.u[iv];
   acc[0] += R * R;
@@ -372,11 +372,13 @@ struct PhasePtrs {
   double* q;
   const double* dsh;   // shared Jacobi / padded shared rows / rowkind flag
   const double* ashe;
+  double* rs;          // this lane's shared-memory residual column (rows <= kLongRow), or null
   bool kinds;          // rows have kinds (element problems)
 };
 
-__device__ __forceinline__ PhasePtrs phase_ptrs(const PropParams& P, size_t vo, size_t ao) {
+__device__ __forceinline__ PhasePtrs phase_ptrs(const PropParams& P, size_t vo, size_t ao, double* rs = nullptr) {
   PhasePtrs Q;
+  Q.rs = rs;
   Q.p = opq(P.p) + vo;
   Q.r = opq(P.r) + vo;
   Q.dinv = opq(P.Dinv) + vo;
@@ -414,7 +416,7 @@ __device__ __forceinline__ void issue_row(const PhasePtrs& Q, const int4* rec, i
   for (int k = 0; k < kEll; ++k) o.pv[k] = Q.p[static_cast<ptrdiff_t>(c[k]) * kLanes];
   const size_t io = static_cast<size_t>(i) * kLanes;
   o.po = Q.p[io];
-  o.ro = Q.r[io];
+  o.ro = (Q.rs != nullptr && o.len <= kLongRow) ? Q.rs[ri * 32] : Q.r[io];
   if (o.shared) {
     o.dv = __ldg(Q.dsh + i);
     const double2* ap = reinterpret_cast<const double2*>(Q.ashe + static_cast<size_t>(i) * kEll);
@@ -488,9 +490,9 @@ struct RowSeq {
 // registers.
 template <bool LINEAR>
 __device__ __forceinline__ void spmv_range(const PropParams& P, const int4* rec, const RowSeq& S, size_t vo,
-                                           size_t ao, double (&acc)[kNDots]) {
+                                           size_t ao, double* rs, double (&acc)[kNDots]) {
   if (S.rb >= S.re) return;
-  const PhasePtrs Q = phase_ptrs(P, vo, ao);
+  const PhasePtrs Q = phase_ptrs(P, vo, ao, rs);
   RowData ra, rc;
   issue_row(Q, rec, S.ri0, S.rb, ra);
   int ri = S.ri0;
@@ -562,7 +564,8 @@ __device__ __forceinline__ void refill_long_rows(const PropParams& P, const ps_c
     if (__ldg(P.long_owner + j) != c) continue;
     const int i = __ldg(P.long_rows + j);
     if (!row_shared(P, i)) {
-      if (warp == 0 && active) refill_row<NPE>(P, curves, i, sys, vo, ao, step, first, acc);
+      if (warp == 0 && active)
+        refill_row<NPE>(P, curves, i, sys, vo, ao, step, first, P.r + vo + static_cast<size_t>(i) * kLanes, acc);
       continue;
     }
     const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
@@ -597,7 +600,7 @@ __device__ __forceinline__ void refill_long_rows(const PropParams& P, const ps_c
         ku += lpart[w][lane];
         mr += lpart2[w][lane];
       }
-      refill_finish(P, i, sys, vo, step, first, true, ku, mr, 0.0, acc);
+      refill_finish(P, i, sys, vo, step, first, true, ku, mr, 0.0, P.r + vo + static_cast<size_t>(i) * kLanes, acc);
     }
     __syncthreads();
   }
@@ -669,6 +672,7 @@ __device__ __forceinline__ void spmv_long_rows(const PropParams& P, bool active,
 // spills inside the persistent kernel, where it is slower.)
 struct BatchB {
   double dv[4], pv[4], qv[4], rv[4], xv[4];
+  bool rsm[4];  // the row's residual lives in shared memory
 };
 
 __device__ __forceinline__ void load_batch_b(const PhasePtrs& Q, const int4* rec, const double* x, const RowSeq& S,
@@ -682,18 +686,21 @@ __device__ __forceinline__ void load_batch_b(const PhasePtrs& Q, const int4* rec
     const int ii = ok ? i : i0;
     const int ri = ok ? r0 + u * S.rstep : r0;
     const size_t io = static_cast<size_t>(ii) * kLanes;
-    const bool sh = !Q.kinds || rec[kRecInts4 * ri].z == 0;
+    const int4 h = rec[kRecInts4 * ri];
+    const bool sh = !Q.kinds || h.z == 0;
     const double* dp = sh ? Q.dsh + ii : Q.dinv + io;
     o.dv[u] = *dp;
     o.pv[u] = Q.p[io];
     o.qv[u] = Q.q[io];
-    o.rv[u] = Q.r[io];
+    o.rsm[u] = Q.rs != nullptr && h.y <= kLongRow;
+    o.rv[u] = o.rsm[u] ? Q.rs[ri * 32] : Q.r[io];
     o.xv[u] = first ? 0.0 : x[io];
   }
 }
 
-__device__ __forceinline__ void store_batch_b(const PhasePtrs& Q, double* x, const RowSeq& S, int i0, double alpha,
-                                              double beta, bool first, const BatchB& o, double (&acc)[kNDots]) {
+__device__ __forceinline__ void store_batch_b(const PhasePtrs& Q, double* x, const RowSeq& S, int i0, int r0,
+                                              double alpha, double beta, bool first, const BatchB& o,
+                                              double (&acc)[kNDots]) {
   double* pw = const_cast<double*>(Q.p);
   double* rw = const_cast<double*>(Q.r);
 #pragma unroll
@@ -704,7 +711,10 @@ __device__ __forceinline__ void store_batch_b(const PhasePtrs& Q, double* x, con
     x[io] = first ? alpha * o.pv[u] : o.xv[u] + alpha * o.pv[u];
     const double r = o.rv[u] - alpha * o.qv[u];
     const double z = o.dv[u] * r;
-    rw[io] = r;
+    if (o.rsm[u])
+      Q.rs[(r0 + u * S.rstep) * 32] = r;
+    else
+      rw[io] = r;
     pw[io] = z + beta * o.pv[u];
     acc[0] += r * r;
     acc[1] += r * z;
@@ -713,16 +723,16 @@ __device__ __forceinline__ void store_batch_b(const PhasePtrs& Q, double* x, con
 
 template <bool LINEAR>
 __device__ __forceinline__ void update_range(const PropParams& P, const int4* rec, double* x, const RowSeq& S,
-                                             size_t vo, double alpha, double beta, bool first,
+                                             size_t vo, double alpha, double beta, bool first, double* rs,
                                              double (&acc)[kNDots]) {
   if (S.rb >= S.re) return;
-  const PhasePtrs Q = phase_ptrs(P, vo, 0);
+  const PhasePtrs Q = phase_ptrs(P, vo, 0, rs);
   double* xb = opq(x) + vo;
   const int bstep = 4 * S.stride, rstep = 4 * S.rstep;
   for (int i0 = S.rb, r0 = S.ri0; i0 < S.re; i0 += bstep, r0 += rstep) {
     BatchB ba;
     load_batch_b(Q, rec, xb, S, i0, r0, first, ba);
-    store_batch_b(Q, xb, S, i0, alpha, beta, first, ba, acc);
+    store_batch_b(Q, xb, S, i0, r0, alpha, beta, first, ba, acc);
   }
 }
 
@@ -746,9 +756,11 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   __shared__ int any_r;  // ... or a refill
   __shared__ double lpart2[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // g: launch-local group (barrier domain); gs: storage group (vectors, systems)
   const int g = blockIdx.x / P.C, c = blockIdx.x % P.C;
+  const int gs = P.g_base + g;
   const int sl = lane;
-  const int sys = g * P.L + sl;
+  const int sys = gs * P.L + sl;
   const bool valid = (sl < P.L) && (sys < P.count);
   if (threadIdx.x < P.ncurves) sh_curves[threadIdx.x] = P.curves[threadIdx.x];
   sync_state_init(sh);
@@ -780,6 +792,10 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   double(*uscr)[kEll][32] = reinterpret_cast<double(*)[kEll][32]>(dyn_smem);
   int4* srec = reinterpret_cast<int4*>(dyn_smem + kScrSmem);
   stage_records(P, c, srec);
+  // the block's residual rows [rec_rows][32] after the records (P.r_smem)
+  double* rsm = P.r_smem ? reinterpret_cast<double*>(dyn_smem + kScrSmem +
+                                                     static_cast<size_t>(P.rec_rows) * kRecInts4 * sizeof(int4))
+                         : nullptr;
   const bool writer = (c == 0) && (warp == 0) && valid;
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
   // Loop-carried state is kept minimal (barrier state and counters in shared
@@ -807,13 +823,14 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     double* xs = LINEAR ? ((step & 1) ? P.ubuf0 : P.ubuf1) : P.x;
     // per-interval addressing from opaque copies of (g, c, warp, lane): the
     // compiler cannot hoist it and keep it live across the whole loop
-    int gq = g, cq = c, wq = warp, lq = sl;
+    int gq = gs, cq = c, wq = warp, lq = sl;
     asm volatile("" : "+r"(gq), "+r"(cq), "+r"(wq), "+r"(lq));
     const size_t vo = static_cast<size_t>(gq) * P.d * kLanes + lq;
     const size_t ao = static_cast<size_t>(gq) * P.nnz * kLanes + lq;
     const RowSeq S = warp_rows(P, cq, wq);
     const int row_begin = S.rb, row_end = S.re, row_step = S.stride;
     const int4* rec = P.rec_rows > 0 ? static_cast<const int4*>(srec) : P.rowrec;
+    double* rs = rsm != nullptr ? rsm + lq : nullptr;  // this lane's residual column
     // ------------------------------------------------ this lane's action
     if (P.n_long > 0 && any_a) {
       if (P.hub_split) {
@@ -827,18 +844,19 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         refill_long_rows<NPE>(P, sh_curves, act == ACT_R0 || act == ACT_R, act == ACT_R0, sys, vo, ao, step, c,
                               lpart, lpart2, acc);
     if (act == ACT_A) {
-      if constexpr (!ODD) spmv_range<LINEAR>(P, rec, S, vo, ao, acc);
+      if constexpr (!ODD) spmv_range<LINEAR>(P, rec, S, vo, ao, rs, acc);
     } else if (act == ACT_B) {
       if constexpr (ODD)
-        update_range<LINEAR>(P, rec, xs, S, vo, lanes[sl].alpha, lanes[sl].beta, lanes[sl].pit == 0, acc);
+        update_range<LINEAR>(P, rec, xs, S, vo, lanes[sl].alpha, lanes[sl].beta, lanes[sl].pit == 0, rs, acc);
     } else if (act == ACT_R0 || act == ACT_R) {
       if (!LINEAR)
         for (int i = row_begin, ri = S.ri0; i < row_end; i += row_step, ri += S.rstep) {
           const int len = rec[kRecInts4 * ri].y;
+          double* rdst = rs != nullptr ? rs + ri * 32 : P.r + vo + static_cast<size_t>(i) * kLanes;
           if (len <= kEll)
-            refill_row_ell<NPE>(P, sh_curves, rec, ri, i, sys, vo, ao, step, act == ACT_R0, uscr[wq], acc);
+            refill_row_ell<NPE>(P, sh_curves, rec, ri, i, sys, vo, ao, step, act == ACT_R0, uscr[wq], rdst, acc);
           else if (len <= kLongRow)
-            refill_row<NPE>(P, sh_curves, i, sys, vo, ao, step, act == ACT_R0, acc);
+            refill_row<NPE>(P, sh_curves, i, sys, vo, ao, step, act == ACT_R0, rdst, acc);
           // longer rows: refill_long_rows
         }
     } else if (act == ACT_U) {
@@ -862,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       // b = M (u/dt) + f, x = 0, r = b, p = D b (proj/src/propagators.cpp:85-94)
       const double* uin = (step & 1) ? P.ubuf1 : P.ubuf0;
       const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
-      for (int i = row_begin; i < row_end; i += row_step) {
+      for (int i = row_begin, ri = S.ri0; i < row_end; i += row_step, ri += S.rstep) {
         const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
         double mv = 0.0;
         for (int k = base; k < end; ++k)
@@ -873,7 +891,10 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         const size_t iv = vo + static_cast<size_t>(i) * kLanes;
         const double z = __ldg(P.Dsh + i) * b;
         xs[iv] = 0.0;
-        P.r[iv] = b;
+        if (rs != nullptr && end - base <= kLongRow)
+          rs[ri * 32] = b;
+        else
+          P.r[iv] = b;
         P.p[iv] = z;
         acc[0] += b * z;
         acc[1] += b * b;
@@ -888,7 +909,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       }
     }
     {
-      const SyncCtx X{P.sync, P.partials, P.abort_flag, P.G, P.C, 32};
+      const SyncCtx X{P.sync, P.partials, P.abort_flag, P.G, P.C, 32, P.L};
       if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, P.dbg ? &t_arr : nullptr)) {
         aborted = true;
         return false;
@@ -914,7 +935,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         // terms to p.q, q.z, q.Dq here, identically in every block; the owner
         // stores it for phase B
         const int hub = __ldg(P.long_rows);
-        const size_t ih = static_cast<size_t>(g) * P.d * kLanes + sl + static_cast<size_t>(hub) * kLanes;
+        const size_t ih = static_cast<size_t>(gs) * P.d * kLanes + sl + static_cast<size_t>(hub) * kLanes;
         const double qh = t3v, ph = P.p[ih], rh = P.r[ih];
         const double dh = row_shared(P, hub) ? __ldg(P.Dsh + hub) : P.Dinv[ih];
         t0v += ph * qh;
@@ -1059,7 +1080,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     o.max_pcg = s.max_pit;
     P.out[sys] = o;
   }
-  if (c == 0 && threadIdx.x == 0) P.lockstep[g] = sh.bar_idx;
+  if (c == 0 && threadIdx.x == 0) P.lockstep[gs] = sh.bar_idx;
   __syncthreads();
   if (P.dbg && threadIdx.x == 0)
     for (int k = 0; k < kDbgSlots; ++k) P.dbg[static_cast<size_t>(blockIdx.x) * kDbgSlots + k] = dbg[k];
@@ -1082,9 +1103,9 @@ __global__ void __launch_bounds__(kThreads, 1) phase_probe_kernel(const PropPara
   const RowSeq S = warp_rows(P, c, warp);
   double acc[kNDots] = {0.0, 0.0, 0.0, 0.0};
   if (mode == 1)
-    spmv_range<false>(P, rec, S, vo, ao, acc);
+    spmv_range<false>(P, rec, S, vo, ao, nullptr, acc);
   else if (mode == 2)
-    update_range<false>(P, rec, P.x, S, vo, 1e-30, 1e-30, false, acc);
+    update_range<false>(P, rec, P.x, S, vo, 1e-30, 1e-30, false, nullptr, acc);
   else {
     // mode 3: the phase-B streams (5 reads, 3 writes) as a flat grid-stride
     // loop over the whole padded batch: the streaming reference for mode 2
@@ -1243,7 +1264,8 @@ int launch_propagate(const PropParams& prm, bool linear, int npe, cudaStream_t s
   void* fn = select_kernel(linear, npe);
   PropParams local = prm;
   void* args[] = {&local};
-  const size_t smem = kScrSmem + static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4);
+  const size_t smem = kScrSmem + static_cast<size_t>(prm.rec_rows) * kRecInts4 * sizeof(int4) +
+                      (prm.r_smem ? static_cast<size_t>(prm.rec_rows) * 32 * sizeof(double) : 0);
   const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(prm.G * prm.C), dim3(kThreads), args, smem, st);
   if (e != cudaSuccess) {
     if (err) *err = std::string("cuda: propagate launch failed: ") + cudaGetErrorString(e);

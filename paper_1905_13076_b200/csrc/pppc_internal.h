@@ -61,6 +61,8 @@ struct PropParams {
   const double* ME;      // [d][kEll] padded mass rows
   const double* KE;      // [d][kEll] padded shared stiffness rows (K linear, K_const element problems)
   int chunk_rot;         // chunk k of kWarps rows belongs to block (k + chunk_rot) mod C
+  int g_base;            // storage group of launch-local group 0 (sequential group launches)
+  int r_smem;            // 1: the PCG residual r of the block's rows (<= kLongRow slots) lives in shared memory
   int pf_dist;           // phase-A L2 prefetch distance in rows; 0 = off
   int hub_split;         // 1: the single long row's phase-A product goes through the reduction
   const double* M;

@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
   X.G = P.G;
   X.C = P.C;
   X.Lp = P.Lp;
+  X.L = P.L;
   const int row_begin = P.warp_row_begin[c * kWarps + warp];
   const int row_end = P.warp_row_begin[c * kWarps + warp + 1];
   const size_t H = static_cast<size_t>(P.H);
