@@ -265,6 +265,7 @@ typedef struct {
   double fine_ms, coarse_ms, spectral_ms, total_ms;
   int64_t fine_pcg_iterations, coarse_pcg_iterations, cocg_iterations, newton_iterations;
   double fine_bytes;               /* canonical algorithmic bytes of the fine kernels */
+  double final_defect;             /* PP-IC: relative_defect(u_N, u_0) of the last iterate */
 } ps_history;
 
 /* solve_pp_pc with the multiharmonic coarse solver [proj/src/engine.cpp:187-270].
@@ -273,6 +274,17 @@ typedef struct {
 int ps_pppc_solve(ps_ctx* fine_ctx, const ps_engine_settings* settings, const double* frozen_ref,
                   double* U_out, double* iterates, ps_history* history);
 int ps_fine_periodicity_defect(ps_ctx* ctx, const double* U, double* defect);
+
+/* classic_parareal [proj/src/engine.cpp:76-129]: initial-value Parareal from u0
+ * (dim) with the context's own problem as fine and coarse propagator.  U_out
+ * is [N+1][dim] (states at T_0..T_N); iterates (or NULL) [max_iterations][N+1][dim]. */
+int ps_classic_parareal(ps_ctx* ctx, const ps_engine_settings* settings, const double* u0,
+                        double* U_out, double* iterates, ps_history* history);
+/* solve_pp_ic [proj/src/engine.cpp:131-185]: periodic Parareal with initial-value
+ * relaxation u_0 <- u_N; converged when jump and relative_defect(u_N, u_0) are
+ * both <= tol.  U_out is [N][dim] (T_0..T_{N-1}); iterates [k][N+1][dim]. */
+int ps_pp_ic_solve(ps_ctx* ctx, const ps_engine_settings* settings, double* U_out,
+                   double* iterates, ps_history* history);
 
 /* Diagnostics: time one PCG phase of the last nonlinear propagation's batch as a
  * standalone (ncu-replayable) kernel: mode 0 = SpMV phase (TMA-staged rows),

@@ -1087,6 +1087,104 @@ int or_pppc_solve(const or_problem* p, const ps_time_mesh* mesh, const ps_solver
   });
 }
 
+// proj/src/engine.cpp:76-129 (classic_parareal) and :131-185 (solve_pp_ic):
+// fine batch over all subintervals, then the sequential coarse sweep with the
+// correction u_n = F_n + (G_new - G_old); the coarse propagator is the same
+// (nonlinear) problem over one coarse step.  U_out holds N + 1 states
+// (classic) or the N states T_0..T_{N-1} (PP-IC); iterates [k][N+1][d].
+namespace {
+int parareal_family(const or_problem* p, const ps_time_mesh* mesh, const ps_solver_settings* s,
+                    const ps_engine_settings* e, int32_t mode, const double* u0, bool periodic, double* U_out,
+                    double* iterates, ps_history* history, int32_t workers) {
+  return guard([&] {
+    if (!(e->tol > 0.0)) throw Error(PS_ERR_BAD_ARG, "engine: tolerance must be positive");
+    if (e->max_iterations < 1) throw Error(PS_ERR_BAD_ARG, "engine: need at least one iteration");
+    if (workers < 1) throw Error(PS_ERR_BAD_ARG, "engine: worker count must be >= 1");
+    const Mesh m = make_mesh(mesh);
+    const Problem& prob = *p->p;
+    const int n_sub = m.N, d = prob.d;
+    const int64_t nd1 = static_cast<int64_t>(n_sub + 1) * d;
+    Propagator prop(prob, m, *s, mode);
+    ps_history h;
+    std::memset(&h, 0, sizeof(h));
+    std::vector<double> u(nd1, 0.0), g_old(static_cast<int64_t>(n_sub) * d), fine_end(static_cast<int64_t>(n_sub) * d),
+        g_new(d);
+    if (!periodic) std::copy(u0, u0 + d, u.begin());
+    {
+      StepOut st;
+      for (int n = 1; n <= n_sub; ++n) {
+        prop.coarse_propagate(n, &u[static_cast<int64_t>(n - 1) * d], &u[static_cast<int64_t>(n) * d], &st);
+        std::copy(&u[static_cast<int64_t>(n) * d], &u[static_cast<int64_t>(n) * d] + d,
+                  &g_old[static_cast<int64_t>(n - 1) * d]);
+      }
+      h.coarse_pcg_iterations += st.pcg;
+    }
+    for (int k = 0; k < e->max_iterations; ++k) {
+      const std::vector<double> u_old = u;
+      std::vector<StepOut> fo(n_sub);
+      parallel_for(n_sub, workers, [&](int i) {
+        prop.fine_propagate(i + 1, &u_old[static_cast<int64_t>(i) * d], &fine_end[static_cast<int64_t>(i) * d],
+                            &fo[i]);
+      });
+      for (int i = 0; i < n_sub; ++i) {
+        h.fine_pcg_iterations += fo[i].pcg;
+        h.newton_iterations += fo[i].iterations;
+      }
+      // periodicity by relaxation (PP-IC): the new period start is the old end
+      if (periodic)
+        std::copy(&u_old[static_cast<int64_t>(n_sub) * d], &u_old[static_cast<int64_t>(n_sub) * d] + d, u.begin());
+      StepOut st;
+      for (int n = 1; n <= n_sub; ++n) {
+        prop.coarse_propagate(n, &u[static_cast<int64_t>(n - 1) * d], g_new.data(), &st);
+        double* un = &u[static_cast<int64_t>(n) * d];
+        const double* fe = &fine_end[static_cast<int64_t>(n - 1) * d];
+        double* go = &g_old[static_cast<int64_t>(n - 1) * d];
+        for (int i = 0; i < d; ++i) {
+          un[i] = fe[i] + (g_new[i] - go[i]);
+          go[i] = g_new[i];
+        }
+      }
+      h.coarse_pcg_iterations += st.pcg;
+      const double jump = jump_norm(n_sub + 1, d, u.data(), u_old.data());
+      if (k < PS_MAX_HISTORY) h.jumps[k] = jump;
+      h.iterations = k + 1;
+      if (iterates) std::copy(u.begin(), u.end(), iterates + static_cast<int64_t>(k) * nd1);
+      bool done = jump <= e->tol;
+      if (periodic) {
+        // relative_defect(u[N], u[0]), proj/src/engine.cpp:26-28
+        const double* w = &u[static_cast<int64_t>(n_sub) * d];
+        double df = 0.0, nw = 0.0;
+        for (int i = 0; i < d; ++i) {
+          df += (w[i] - u[i]) * (w[i] - u[i]);
+          nw += w[i] * w[i];
+        }
+        h.final_defect = std::sqrt(df) / std::max(1.0, std::sqrt(nw));
+        done = done && h.final_defect <= e->tol;
+      }
+      if (done) {
+        h.converged = 1;
+        break;
+      }
+    }
+    std::copy(u.begin(), u.begin() + (periodic ? nd1 - d : nd1), U_out);
+    if (history) *history = h;
+  });
+}
+}  // namespace
+
+int or_classic_parareal(const or_problem* p, const ps_time_mesh* mesh, const ps_solver_settings* s,
+                        const ps_engine_settings* e, int32_t mode, const double* u0, double* U_out, double* iterates,
+                        ps_history* history, int32_t workers) {
+  if (!u0) return PS_ERR_BAD_ARG;
+  return parareal_family(p, mesh, s, e, mode, u0, false, U_out, iterates, history, workers);
+}
+
+int or_pp_ic_solve(const or_problem* p, const ps_time_mesh* mesh, const ps_solver_settings* s,
+                   const ps_engine_settings* e, int32_t mode, double* U_out, double* iterates, ps_history* history,
+                   int32_t workers) {
+  return parareal_family(p, mesh, s, e, mode, nullptr, true, U_out, iterates, history, workers);
+}
+
 // proj/src/engine.cpp:272-290
 int or_fine_periodicity_defect(const or_problem* p, const ps_time_mesh* mesh, const ps_solver_settings* s,
                                int32_t mode, const double* U, double* defect, int32_t workers) {

@@ -85,6 +85,12 @@ double or_jump_norm(int32_t count, int32_t d, const double* cur, const double* p
 int or_pppc_solve(const or_problem* p, const ps_time_mesh* mesh, const ps_solver_settings* s,
                   const ps_engine_settings* e, int32_t mode, const double* frozen_ref,
                   double* U_out, double* iterates, ps_history* history, int32_t workers);
+int or_classic_parareal(const or_problem* p, const ps_time_mesh* mesh, const ps_solver_settings* s,
+                        const ps_engine_settings* e, int32_t mode, const double* u0, double* U_out,
+                        double* iterates, ps_history* history, int32_t workers);
+int or_pp_ic_solve(const or_problem* p, const ps_time_mesh* mesh, const ps_solver_settings* s,
+                   const ps_engine_settings* e, int32_t mode, double* U_out, double* iterates,
+                   ps_history* history, int32_t workers);
 int or_fine_periodicity_defect(const or_problem* p, const ps_time_mesh* mesh,
                                const ps_solver_settings* s, int32_t mode, const double* U,
                                double* defect, int32_t workers);

@@ -59,6 +59,12 @@ _SIG = {
     "or_pppc_solve": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh), C.POINTER(_abi.ps_solver_settings),
                                 C.POINTER(_abi.ps_engine_settings), C.c_int32, dp, dp, dp,
                                 C.POINTER(_abi.ps_history), C.c_int32]),
+    "or_classic_parareal": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh), C.POINTER(_abi.ps_solver_settings),
+                                      C.POINTER(_abi.ps_engine_settings), C.c_int32, dp, dp, dp,
+                                      C.POINTER(_abi.ps_history), C.c_int32]),
+    "or_pp_ic_solve": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh), C.POINTER(_abi.ps_solver_settings),
+                                 C.POINTER(_abi.ps_engine_settings), C.c_int32, dp, dp,
+                                 C.POINTER(_abi.ps_history), C.c_int32]),
     "or_fine_periodicity_defect": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh),
                                              C.POINTER(_abi.ps_solver_settings), C.c_int32, dp, dp, C.c_int32]),
     "or_sequential_steady_state": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh),
@@ -230,6 +236,37 @@ class Oracle:
                     fine_pcg_iterations=h.fine_pcg_iterations, coarse_pcg_iterations=h.coarse_pcg_iterations,
                     cocg_iterations=h.cocg_iterations, newton_iterations=h.newton_iterations)
         return U, hist, (its[:h.iterations] if its is not None else None)
+
+    def _parareal(self, settings, u0, mode, keep_iterates, workers):
+        mesh = settings.mesh
+        s = self._s(settings.newton, settings.pcg, settings.cocg)
+        m = mesh.c()
+        e = _abi.ps_engine_settings()
+        e.tol, e.max_iterations = settings.tol, settings.max_iterations
+        n1 = mesh.subintervals + 1
+        its = np.empty((settings.max_iterations, n1, self.dim)) if keep_iterates else None
+        h = _abi.ps_history()
+        if u0 is None:
+            U = np.empty((mesh.subintervals, self.dim))
+            _check(lib().or_pp_ic_solve(self._h, C.byref(m), C.byref(s), C.byref(e), mode, _p(U), _p(its),
+                                        C.byref(h), workers or workers_default()))
+        else:
+            U = np.empty((n1, self.dim))
+            _check(lib().or_classic_parareal(self._h, C.byref(m), C.byref(s), C.byref(e), mode, _p(_f(u0)), _p(U),
+                                             _p(its), C.byref(h), workers or workers_default()))
+        hist = dict(iterations=h.iterations, converged=bool(h.converged),
+                    jumps=[h.jumps[k] for k in range(min(h.iterations, _abi.PS_MAX_HISTORY))],
+                    final_defect=h.final_defect, fine_pcg_iterations=h.fine_pcg_iterations,
+                    coarse_pcg_iterations=h.coarse_pcg_iterations, newton_iterations=h.newton_iterations)
+        return U, hist, (its[:h.iterations] if its is not None else None)
+
+    def classic_parareal(self, settings: EngineSettings, u0, mode=ITERATIVE, keep_iterates=False, workers=None):
+        """proj/src/engine.cpp:76-129: states [N+1][d]."""
+        return self._parareal(settings, u0, mode, keep_iterates, workers)
+
+    def solve_pp_ic(self, settings: EngineSettings, mode=ITERATIVE, keep_iterates=False, workers=None):
+        """proj/src/engine.cpp:131-185: trajectory [N][d] (T_0..T_{N-1})."""
+        return self._parareal(settings, None, mode, keep_iterates, workers)
 
     def fine_periodicity_defect(self, mesh, U, newton=None, pcg=None, mode=ITERATIVE, workers=None):
         s = self._s(newton, pcg)

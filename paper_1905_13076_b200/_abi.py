@@ -91,7 +91,8 @@ class ps_history(C.Structure):
                 ("fine_ms", C.c_double), ("coarse_ms", C.c_double), ("spectral_ms", C.c_double),
                 ("total_ms", C.c_double), ("fine_pcg_iterations", C.c_int64),
                 ("coarse_pcg_iterations", C.c_int64), ("cocg_iterations", C.c_int64),
-                ("newton_iterations", C.c_int64), ("fine_bytes", C.c_double)]
+                ("newton_iterations", C.c_int64), ("fine_bytes", C.c_double),
+                ("final_defect", C.c_double)]
 
 
 class ps_polar_cable_params(C.Structure):
@@ -147,6 +148,8 @@ _SIGNATURES = {
     "ps_eval_reluctivity": (C.c_int, [C.POINTER(ps_curve), C.c_int32, dp, dp, dp]),
     "ps_pppc_solve": (C.c_int, [vp, C.POINTER(ps_engine_settings), dp, dp, dp, C.POINTER(ps_history)]),
     "ps_fine_periodicity_defect": (C.c_int, [vp, dp, dp]),
+    "ps_classic_parareal": (C.c_int, [vp, C.POINTER(ps_engine_settings), dp, dp, dp, C.POINTER(ps_history)]),
+    "ps_pp_ic_solve": (C.c_int, [vp, C.POINTER(ps_engine_settings), dp, dp, C.POINTER(ps_history)]),
     "ps_polar_cable_defaults": (C.c_int, [C.POINTER(ps_polar_cable_params)]),
     "ps_build_polar_cable": (C.c_int, [C.POINTER(ps_polar_cable_params), C.POINTER(vp)]),
     "ps_radial_cable_defaults": (C.c_int, [C.POINTER(ps_radial_cable_params)]),

@@ -645,6 +645,57 @@ def solve_pp_pc(problem: PeriodicProblem, settings: EngineSettings, keep_iterate
         prop.close()
 
 
+@dataclass
+class InitialValueSolveResult:
+    states: np.ndarray              # [N+1][d] states at T_0..T_N
+    history: dict
+    iterates: Optional[np.ndarray] = None
+
+
+def _parareal_family(problem: PeriodicProblem, settings: EngineSettings, u0, keep_iterates: bool,
+                     stream: Optional[int]):
+    mesh = settings.mesh
+    if u0 is not None:
+        u0 = _f64(u0).reshape(-1)
+        if u0.shape[0] != problem.dim:
+            raise ParasteadyError(_abi.PS_ERR_BAD_ARG, "engine: initial state dimension mismatch")
+    prop = Propagator(problem, mesh, settings.newton, settings.pcg, settings.cocg, stream=stream)
+    try:
+        e = _abi.ps_engine_settings()
+        e.tol = settings.tol
+        e.max_iterations = settings.max_iterations
+        n1 = mesh.subintervals + 1
+        its = np.empty((settings.max_iterations, n1, problem.dim)) if keep_iterates else None
+        h = _abi.ps_history()
+        if u0 is None:
+            U = np.empty((mesh.subintervals, problem.dim))
+            rc = lib().ps_pp_ic_solve(prop._ctx, C.byref(e), _dp(U), _dp(its), C.byref(h))
+        else:
+            U = np.empty((n1, problem.dim))
+            rc = lib().ps_classic_parareal(prop._ctx, C.byref(e), _dp(u0), _dp(U), _dp(its), C.byref(h))
+        _raise(rc, prop._ctx)
+        hist = dict(iterations=h.iterations, converged=bool(h.converged),
+                    jumps=[h.jumps[k] for k in range(min(h.iterations, _abi.PS_MAX_HISTORY))],
+                    final_defect=h.final_defect, fine_ms=h.fine_ms, coarse_ms=h.coarse_ms, total_ms=h.total_ms,
+                    fine_pcg_iterations=h.fine_pcg_iterations, coarse_pcg_iterations=h.coarse_pcg_iterations,
+                    newton_iterations=h.newton_iterations, fine_bytes=h.fine_bytes)
+        return U, hist, (its[:h.iterations] if its is not None else None)
+    finally:
+        prop.close()
+
+
+def classic_parareal(problem: PeriodicProblem, u0, settings: EngineSettings, keep_iterates: bool = False,
+                     stream: Optional[int] = None) -> InitialValueSolveResult:
+    """Initial-value Parareal (proj/src/engine.cpp:76-129), driven by ps_classic_parareal."""
+    return InitialValueSolveResult(*_parareal_family(problem, settings, u0, keep_iterates, stream))
+
+
+def solve_pp_ic(problem: PeriodicProblem, settings: EngineSettings, keep_iterates: bool = False,
+                stream: Optional[int] = None) -> PeriodicSolveResult:
+    """PP-IC (proj/src/engine.cpp:131-185), driven by ps_pp_ic_solve."""
+    return PeriodicSolveResult(*_parareal_family(problem, settings, None, keep_iterates, stream))
+
+
 def fine_periodicity_defect(problem: PeriodicProblem, trajectory, mesh: TimeMesh,
                             newton: Optional[NewtonSettings] = None) -> float:
     """proj/src/engine.cpp:272-290."""

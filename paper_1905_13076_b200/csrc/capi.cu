@@ -1406,6 +1406,178 @@ int ps_pppc_solve(ps_ctx* fine, const ps_engine_settings* settings, const double
   return rc;
 }
 
+// ------------------------------------------------ classical Parareal and PP-IC
+// proj/src/engine.cpp:76-129 (classic_parareal) and :131-185 (solve_pp_ic):
+// the fine batch runs as one batched launch over all N subintervals; the coarse
+// sweep is inherently sequential (u_n needs the corrected u_{n-1}) and runs one
+// single-system coarse step per subinterval, each followed by the fused
+// correction u_n = F_n + (G_new - G_old), G_old <- G_new.  States stay in HBM
+// in the reference's [N+1][d] order; the host reads one jump (and for PP-IC one
+// defect) per iteration.
+}  // extern "C"
+
+namespace {
+
+__global__ void parareal_correct_kernel(const double* __restrict__ fine_end, const double* __restrict__ g_new,
+                                        double* __restrict__ g_old, double* __restrict__ u_n, int d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d) return;
+  const double gn = g_new[i];
+  u_n[i] = fine_end[i] + (gn - g_old[i]);
+  g_old[i] = gn;
+}
+
+// part[n] = (|cur_n - prev_n|^2, |cur_n|^2) for row-major [count][d] states
+__global__ void row_jump_kernel(const double* cur, const double* prev, int d, double* part) {
+  __shared__ double sa[256], sb[256];
+  const int n = blockIdx.x;
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const size_t k = static_cast<size_t>(n) * d + i;
+    const double c = cur[k], df = c - prev[k];
+    a += df * df;
+    b += c * c;
+  }
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (static_cast<int>(threadIdx.x) < w) {
+      sa[threadIdx.x] += sa[threadIdx.x + w];
+      sb[threadIdx.x] += sb[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * n] = sa[0];
+    part[2 * n + 1] = sb[0];
+  }
+}
+
+// jump_norm (proj/src/engine.cpp:54-64) over `count` row-major states
+double row_jump(const double* cur, const double* prev, int count, int d, double* part, cudaStream_t st) {
+  row_jump_kernel<<<count, 256, 0, st>>>(cur, prev, d, part);
+  std::vector<double> h(static_cast<size_t>(2) * count);
+  check(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "jump");
+  check(cudaStreamSynchronize(st), "jump");
+  double change = 0.0, scale = 1.0;
+  for (int n = 0; n < count; ++n) {
+    change = std::max(change, std::sqrt(h[2 * n]));
+    scale = std::max(scale, std::sqrt(h[2 * n + 1]));
+  }
+  return change / scale;
+}
+
+int parareal_family(ps_ctx* ctx, const ps_engine_settings* settings, const double* u0, bool periodic, double* U_out,
+                    double* iterates, ps_history* history) {
+  if (!ctx || !settings || !U_out || (!periodic && !u0)) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    if (!(settings->tol > 0.0)) throw Failure(PS_ERR_BAD_ARG, "engine: tolerance must be positive");
+    if (settings->max_iterations < 1) throw Failure(PS_ERR_BAD_ARG, "engine: need at least one iteration");
+    const int N = ctx->mesh.subintervals, d = ctx->P.d;
+    if (ctx->max_batch < N) throw Failure(PS_ERR_BAD_ARG, "engine: context batch smaller than N");
+    cudaStream_t st = ctx->stream;
+    const size_t nd = static_cast<size_t>(N) * d, nd1 = nd + d;
+    double *U = nullptr, *Uold = nullptr, *F = nullptr, *Gold = nullptr, *gnew = nullptr, *part = nullptr;
+    if (!dalloc(&U, nd1) || !dalloc(&Uold, nd1) || !dalloc(&F, nd) || !dalloc(&Gold, nd) || !dalloc(&gnew, d) ||
+        !dalloc(&part, 2 * static_cast<size_t>(N + 1)))
+      throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+    std::unique_ptr<double, cudaError_t (*)(void*)> h0(U, cudaFree), h1(Uold, cudaFree), h2(F, cudaFree),
+        h3(Gold, cudaFree), h4(gnew, cudaFree), h5(part, cudaFree);
+    ps_history h;
+    std::memset(&h, 0, sizeof(h));
+    cudaEvent_t t0, t1;
+    check(cudaEventCreate(&t0), "event");
+    check(cudaEventCreate(&t1), "event");
+    check(cudaEventRecord(t0, st), "event");
+    check(cudaMemsetAsync(U, 0, nd1 * sizeof(double), st), "init");
+    if (!periodic) check(cudaMemcpyAsync(U, u0, d * sizeof(double), cudaMemcpyHostToDevice, st), "u0");
+    const double dT = coarse_dt(ctx->mesh), dt = fine_dt(ctx->mesh);
+    const int cblocks = (d + 255) / 256;
+    // one coarse step G_n(U[n-1]) into gnew (proj/src/propagators.cpp:107-115)
+    auto coarse_step = [&](int n) {
+      stage_in_dev(ctx, U + static_cast<size_t>(n - 1) * d, 1);
+      ps_batch_status cs{};
+      PropResult r = propagate(ctx, 1, 1, dT, std::vector<double>{boundary(ctx->mesh, n)}, false, false, &cs);
+      launch_from_blocked(r.state, gnew, 1, d, 1, st);
+      h.coarse_ms += cs.kernel_ms;
+      h.coarse_pcg_iterations += cs.pcg_iterations;
+    };
+    for (int n = 1; n <= N; ++n) {
+      coarse_step(n);
+      check(cudaMemcpyAsync(U + static_cast<size_t>(n) * d, gnew, d * sizeof(double), cudaMemcpyDeviceToDevice, st),
+            "sweep");
+      check(cudaMemcpyAsync(Gold + static_cast<size_t>(n - 1) * d, gnew, d * sizeof(double),
+                            cudaMemcpyDeviceToDevice, st),
+            "sweep");
+    }
+    for (int k = 0; k < settings->max_iterations; ++k) {
+      check(cudaMemcpyAsync(Uold, U, nd1 * sizeof(double), cudaMemcpyDeviceToDevice, st), "u_old");
+      // fine batch F_n(u_old[n-1]), n = 1..N, one launch
+      stage_in_dev(ctx, Uold, N);
+      ps_batch_status fs{};
+      PropResult fr = propagate(ctx, N, ctx->mesh.fine_steps, dt, fine_times(ctx->mesh, 1, N), false, false, &fs);
+      launch_from_blocked(fr.state, F, N, d, lanes_per_group(N), st);
+      h.fine_ms += fs.kernel_ms;
+      h.fine_pcg_iterations += fs.pcg_iterations;
+      h.newton_iterations += fs.newton_iterations;
+      h.fine_bytes += fs.algorithmic_bytes;
+      // periodicity by relaxation (PP-IC): the new period start is the old end
+      if (periodic)
+        check(cudaMemcpyAsync(U, Uold + nd, d * sizeof(double), cudaMemcpyDeviceToDevice, st), "relax");
+      for (int n = 1; n <= N; ++n) {
+        coarse_step(n);
+        parareal_correct_kernel<<<cblocks, 256, 0, st>>>(F + static_cast<size_t>(n - 1) * d, gnew,
+                                                         Gold + static_cast<size_t>(n - 1) * d,
+                                                         U + static_cast<size_t>(n) * d, d);
+      }
+      const double jump = row_jump(U, Uold, N + 1, d, part, st);
+      if (k < PS_MAX_HISTORY) h.jumps[k] = jump;
+      h.iterations = k + 1;
+      if (iterates) {
+        check(cudaMemcpyAsync(iterates + static_cast<size_t>(k) * nd1, U, nd1 * sizeof(double),
+                              cudaMemcpyDeviceToHost, st),
+              "iterate");
+        check(cudaStreamSynchronize(st), "iterate");
+      }
+      bool done = jump <= settings->tol;
+      if (periodic) {
+        // relative_defect(u_N, u_0) (proj/src/engine.cpp:26-28)
+        h.final_defect = row_jump(U + nd, U, 1, d, part, st);
+        done = done && h.final_defect <= settings->tol;
+      }
+      if (done) {
+        h.converged = 1;
+        break;
+      }
+    }
+    check(cudaEventRecord(t1, st), "event");
+    check(cudaMemcpyAsync(U_out, U, (periodic ? nd : nd1) * sizeof(double), cudaMemcpyDeviceToHost, st), "U_out");
+    check(cudaStreamSynchronize(st), "U_out");
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    h.total_ms = ms;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (history) *history = h;
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int ps_classic_parareal(ps_ctx* ctx, const ps_engine_settings* settings, const double* u0, double* U_out,
+                        double* iterates, ps_history* history) {
+  return parareal_family(ctx, settings, u0, false, U_out, iterates, history);
+}
+
+int ps_pp_ic_solve(ps_ctx* ctx, const ps_engine_settings* settings, double* U_out, double* iterates,
+                   ps_history* history) {
+  return parareal_family(ctx, settings, nullptr, true, U_out, iterates, history);
+}
+
 // fine_periodicity_defect (proj/src/engine.cpp:272-290)
 // Diagnostic: time one PCG phase of the last nonlinear propagation's batch as a
 // standalone kernel (see phase_probe_kernel).  mode 0 = phase A (TMA-staged),

@@ -32,7 +32,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_abi.ps_problem_desc) == 144
     assert C.sizeof(_abi.ps_batch_status) == 72
     assert C.sizeof(_abi.ps_newton_settings) == 32
-    assert C.sizeof(_abi.ps_history) == 8 + 8 * 256 + 4 * 8 + 4 * 8 + 8
+    assert C.sizeof(_abi.ps_history) == 8 + 8 * 256 + 4 * 8 + 4 * 8 + 8 + 8  # + final_defect
 
 
 def test_default_settings_are_reference_defaults():

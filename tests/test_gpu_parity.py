@@ -298,3 +298,57 @@ def test_pppc_config1_matches_oracle():
     for k in range(hist_o["iterations"]):
         assert rel_l2(res.iterates[k], its_o[k]) <= TOL, k
     assert rel_l2(res.trajectory, U_o) <= TOL
+
+
+# ------------------------------------- §8(f) rank 1: classic Parareal, PP-IC
+def test_classic_parareal_exact_termination_bitwise():
+    """proj/tests/test_engine.cpp:141-165 on the device: exact cancellation
+    ends the iteration within N + 1 iterations on the sequential fine solution,
+    bit for bit (the batched fine launch equals the one-system launches)."""
+    p = ps.build_dae_pair()
+    mesh = ps.TimeMesh(6, 4, p.period)
+    es = ps.EngineSettings(mesh, tol=1e-300, max_iterations=mesh.subintervals + 2)
+    u0 = np.array([0.3, -0.2])
+    res = ps.classic_parareal(p, u0, es, keep_iterates=True)
+    h = res.history
+    assert h["converged"] and h["iterations"] <= mesh.subintervals + 1
+    assert h["jumps"][-1] == 0.0
+    prop = ps.Propagator(p, mesh)
+    u = [u0]
+    for n in range(1, mesh.subintervals + 1):
+        u.append(prop.fine_propagate(n, u[-1]))
+    assert np.array_equal(res.states, np.stack(u))
+    U_o, h_o, its_o = po.Oracle(p).classic_parareal(es, u0, mode=po.ITERATIVE, keep_iterates=True)
+    assert h["iterations"] == h_o["iterations"]
+    for k in range(h_o["iterations"]):
+        assert rel_l2(res.iterates[k], its_o[k]) <= TOL, k
+
+
+def test_classic_parareal_nonlinear_polar_matches_oracle():
+    prob = small_polar()
+    mesh = ps.TimeMesh(6, 3, prob.period)
+    es = ps.EngineSettings(mesh, tol=1e-10, max_iterations=10, newton=NEWTON_BASELINE)
+    u0 = ps.seeded_normal(3, prob.dim, 1e-3)
+    res = ps.classic_parareal(prob, u0, es, keep_iterates=True)
+    U_o, h_o, its_o = po.Oracle(prob).classic_parareal(es, u0, mode=po.ITERATIVE, keep_iterates=True)
+    assert res.history["converged"] and h_o["converged"]
+    assert res.history["iterations"] == h_o["iterations"]
+    for k in range(h_o["iterations"]):
+        assert rel_l2(res.iterates[k], its_o[k]) <= TOL, k
+
+
+def test_pp_ic_nonlinear_radial_cable_matches_oracle():
+    """PP-IC on the reference's nonlinear cable (n_r = 41, N = 4, s = 10)."""
+    cable = ps.build_coax_cable(n_r=41)
+    mesh = ps.TimeMesh(4, 10, cable.period)
+    es = ps.EngineSettings(mesh, tol=1e-8, max_iterations=200)
+    res = ps.solve_pp_ic(cable, es, keep_iterates=True)
+    U_o, h_o, its_o = po.Oracle(cable).solve_pp_ic(es, mode=po.ITERATIVE, keep_iterates=True)
+    assert res.history["converged"] and h_o["converged"]
+    assert res.history["iterations"] == h_o["iterations"]
+    assert res.history["final_defect"] <= 1e-8
+    for k in range(0, h_o["iterations"], 5):
+        assert rel_l2(res.iterates[k], its_o[k]) <= TOL, k
+    assert rel_l2(res.trajectory, U_o) <= TOL
+    pc = ps.solve_pp_pc(cable, ps.EngineSettings(mesh, tol=1e-8, max_iterations=10))
+    assert pc.history["iterations"] < res.history["iterations"]

@@ -282,3 +282,79 @@ def test_line_search_extension_rescues_deep_saturation():
     F = orc.fine_propagate_batch(mesh, 1, u0, newton=NEWTON_BASELINE, mode=po.DIRECT)
     Fi = orc.fine_propagate_batch(mesh, 1, u0, newton=NEWTON_BASELINE, mode=po.ITERATIVE)
     assert rel_l2(Fi, F) <= 1e-9
+
+
+# ------------------------------------------- §8(f) rank 1: Parareal and PP-IC
+def _sequential_fine(orc, mesh, u0, mode=po.DIRECT):
+    u = [np.asarray(u0, dtype=np.float64)]
+    for n in range(1, mesh.subintervals + 1):
+        u.append(orc.fine_propagate_batch(mesh, n, u[-1].reshape(1, -1), mode=mode)[0])
+    return np.stack(u)
+
+
+def test_classic_parareal_zero_excitation_fixed_point():
+    """proj/tests/test_engine.cpp:126-133."""
+    p = ps.build_scalar_test(1.0, 1.0, 0.0, 50.0)
+    U, h, _ = po.Oracle(p).classic_parareal(ps.EngineSettings(ps.TimeMesh(6, 4, p.period)), np.zeros(1))
+    assert h["converged"] and h["iterations"] == 1
+    assert np.all(U == 0.0)
+
+
+def test_classic_parareal_s1_one_iteration():
+    """proj/tests/test_engine.cpp:134-140."""
+    p = ps.build_dae_pair()
+    U, h, _ = po.Oracle(p).classic_parareal(ps.EngineSettings(ps.TimeMesh(6, 1, p.period)), np.zeros(2))
+    assert h["converged"] and h["iterations"] == 1
+
+
+@pytest.mark.parametrize("mode", [po.DIRECT, po.ITERATIVE])
+def test_classic_parareal_exact_termination(mode):
+    """proj/tests/test_engine.cpp:141-165: with an unreachable tolerance the
+    iteration stops on exact cancellation within N + 1 iterations, on the
+    sequential fine solution bit for bit."""
+    p = ps.build_dae_pair()
+    mesh = ps.TimeMesh(6, 4, p.period)
+    es = ps.EngineSettings(mesh, tol=1e-300, max_iterations=mesh.subintervals + 2)
+    u0 = np.array([0.3, -0.2])
+    orc = po.Oracle(p)
+    U, h, _ = orc.classic_parareal(es, u0, mode=mode)
+    assert h["converged"] and h["iterations"] <= mesh.subintervals + 1
+    assert h["jumps"][-1] == 0.0
+    assert np.array_equal(U, _sequential_fine(orc, mesh, u0, mode))
+
+
+def test_classic_parareal_exactness_acceptance4():
+    """Acceptance [4] (proj/tests/acceptance_main.cpp:165-191)."""
+    p = ps.build_scalar_test(1.0, 1.0, 1.0, 50.0)
+    mesh = ps.TimeMesh(10, 20, p.period)
+    orc = po.Oracle(p)
+    U, h, _ = orc.classic_parareal(ps.EngineSettings(mesh, tol=1e-300, max_iterations=10), np.zeros(1))
+    F = _sequential_fine(orc, mesh, np.zeros(1))
+    rel = np.max(np.linalg.norm(U - F, axis=1)) / max(1.0, np.max(np.linalg.norm(F, axis=1)))
+    assert rel <= 1e-12
+
+
+def test_pp_ic_needs_more_iterations_than_pp_pc_acceptance7():
+    """Acceptance [7] (proj/tests/acceptance_main.cpp:243-275): linear radial
+    cable, N = 20, s = 100, tol 1e-6: PP-PC within 5 iterations, PP-IC strictly
+    more, both on the same periodic orbit."""
+    cable = ps.build_coax_cable(linear_sleeve=True)
+    mesh = ps.TimeMesh(20, 100, cable.period)
+    orc = po.Oracle(cable)
+    U_pc, h_pc, _ = orc.solve_pp_pc(ps.EngineSettings(mesh, tol=1e-6), mode=po.DIRECT)
+    U_ic, h_ic, _ = orc.solve_pp_ic(ps.EngineSettings(mesh, tol=1e-6, max_iterations=500), mode=po.DIRECT)
+    assert h_pc["converged"] and h_pc["iterations"] <= 5
+    assert h_ic["converged"] and h_ic["iterations"] > h_pc["iterations"]
+    assert h_ic["final_defect"] <= 1e-6
+    scale = max(1.0, np.max(np.linalg.norm(U_pc, axis=1)))
+    assert np.max(np.linalg.norm(U_ic - U_pc, axis=1)) / scale <= 1e-4
+
+
+def test_parareal_settings_validation():
+    """proj/tests/test_engine.cpp:104-123."""
+    p = ps.build_dae_pair()
+    orc = po.Oracle(p)
+    with pytest.raises(ps.ParasteadyError, match="tolerance"):
+        orc.solve_pp_ic(ps.EngineSettings(ps.TimeMesh(4, 2, p.period), tol=0.0))
+    with pytest.raises(ps.ParasteadyError, match="iteration"):
+        orc.classic_parareal(ps.EngineSettings(ps.TimeMesh(4, 2, p.period), max_iterations=0), np.zeros(2))
