@@ -285,6 +285,10 @@ int ps_classic_parareal(ps_ctx* ctx, const ps_engine_settings* settings, const d
  * both <= tol.  U_out is [N][dim] (T_0..T_{N-1}); iterates [k][N+1][dim]. */
 int ps_pp_ic_solve(ps_ctx* ctx, const ps_engine_settings* settings, double* U_out,
                    double* iterates, ps_history* history);
+/* sequential_steady_state [proj/src/propagators.cpp:117-149]: U_out [N][dim] holds
+ * the last period's states T_0..T_{N-1}; defects (or NULL) [max_periods]. */
+int ps_sequential_steady_state(ps_ctx* ctx, double tol, int32_t max_periods, double* U_out,
+                               int32_t* periods, int32_t* converged, double* defects);
 
 /* Diagnostics: time one PCG phase of the last nonlinear propagation's batch as a
  * standalone (ncu-replayable) kernel: mode 0 = SpMV phase (TMA-staged rows),

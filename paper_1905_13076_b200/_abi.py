@@ -150,6 +150,7 @@ _SIGNATURES = {
     "ps_fine_periodicity_defect": (C.c_int, [vp, dp, dp]),
     "ps_classic_parareal": (C.c_int, [vp, C.POINTER(ps_engine_settings), dp, dp, dp, C.POINTER(ps_history)]),
     "ps_pp_ic_solve": (C.c_int, [vp, C.POINTER(ps_engine_settings), dp, dp, C.POINTER(ps_history)]),
+    "ps_sequential_steady_state": (C.c_int, [vp, C.c_double, C.c_int32, dp, ip, ip, dp]),
     "ps_polar_cable_defaults": (C.c_int, [C.POINTER(ps_polar_cable_params)]),
     "ps_build_polar_cable": (C.c_int, [C.POINTER(ps_polar_cable_params), C.POINTER(vp)]),
     "ps_radial_cable_defaults": (C.c_int, [C.POINTER(ps_radial_cable_params)]),

@@ -696,6 +696,30 @@ def solve_pp_ic(problem: PeriodicProblem, settings: EngineSettings, keep_iterate
     return PeriodicSolveResult(*_parareal_family(problem, settings, None, keep_iterates, stream))
 
 
+@dataclass
+class SteadyStateResult:
+    trajectory: np.ndarray          # [N][d] last period's states T_0..T_{N-1}
+    periods: int
+    converged: bool
+    period_defects: list
+
+
+def sequential_steady_state(problem: PeriodicProblem, mesh: TimeMesh, tol: float, max_periods: int,
+                            newton: Optional[NewtonSettings] = None,
+                            pcg: Optional[KrylovSettings] = None) -> SteadyStateResult:
+    """Brute-force periodic steady state (proj/src/propagators.cpp:117-149) on the device."""
+    prop = Propagator(problem, mesh, newton, pcg)
+    try:
+        U = np.empty((mesh.subintervals, problem.dim))
+        per, conv = C.c_int32(0), C.c_int32(0)
+        defects = np.zeros(max(1, int(max_periods)))
+        prop._check(lib().ps_sequential_steady_state(prop._ctx, float(tol), int(max_periods), _dp(U), C.byref(per),
+                                                     C.byref(conv), _dp(defects)))
+        return SteadyStateResult(U, per.value, bool(conv.value), list(defects[:per.value]))
+    finally:
+        prop.close()
+
+
 def fine_periodicity_defect(problem: PeriodicProblem, trajectory, mesh: TimeMesh,
                             newton: Optional[NewtonSettings] = None) -> float:
     """proj/src/engine.cpp:272-290."""

@@ -1578,6 +1578,48 @@ int ps_pp_ic_solve(ps_ctx* ctx, const ps_engine_settings* settings, double* U_ou
   return parareal_family(ctx, settings, nullptr, true, U_out, iterates, history);
 }
 
+// sequential_steady_state (proj/src/propagators.cpp:117-149): period after
+// period from zero, one fine propagation per subinterval (batch size 1), until
+// the period map's relative defect is <= tol.  U_out [N][dim]: the last
+// period's states T_0..T_{N-1}; defects [max_periods] or NULL.
+int ps_sequential_steady_state(ps_ctx* ctx, double tol, int32_t max_periods, double* U_out, int32_t* periods,
+                               int32_t* converged, double* defects) {
+  if (!ctx || !U_out || !periods || !converged) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    if (!(tol > 0.0)) throw Failure(PS_ERR_BAD_ARG, "propagator: tolerance must be positive");
+    if (max_periods < 1) throw Failure(PS_ERR_BAD_ARG, "propagator: need at least one period");
+    const int N = ctx->mesh.subintervals, d = ctx->P.d;
+    cudaStream_t st = ctx->stream;
+    const size_t nd = static_cast<size_t>(N) * d;
+    double *traj = nullptr, *part = nullptr;
+    if (!dalloc(&traj, nd + d) || !dalloc(&part, 2)) throw Failure(PS_ERR_CUDA, "cuda: out of memory");
+    std::unique_ptr<double, cudaError_t (*)(void*)> h0(traj, cudaFree), h1(part, cudaFree);
+    check(cudaMemsetAsync(traj, 0, (nd + d) * sizeof(double), st), "init");
+    const double dt = fine_dt(ctx->mesh);
+    *converged = 0;
+    for (int per = 1; per <= max_periods; ++per) {
+      for (int n = 1; n <= N; ++n) {
+        stage_in_dev(ctx, traj + static_cast<size_t>(n - 1) * d, 1);
+        ps_batch_status fs{};
+        PropResult r = propagate(ctx, 1, ctx->mesh.fine_steps, dt, fine_times(ctx->mesh, n, 1), false, false, &fs);
+        launch_from_blocked(r.state, traj + static_cast<size_t>(n) * d, 1, d, 1, st);
+      }
+      // (u_end - u).norm() / max(1, u_end.norm())
+      const double defect = row_jump(traj + nd, traj, 1, d, part, st);
+      if (defects) defects[per - 1] = defect;
+      *periods = per;
+      check(cudaMemcpyAsync(U_out, traj, nd * sizeof(double), cudaMemcpyDeviceToHost, st), "U_out");
+      check(cudaMemcpyAsync(traj, traj + nd, d * sizeof(double), cudaMemcpyDeviceToDevice, st), "wrap");
+      check(cudaStreamSynchronize(st), "U_out");
+      if (defect <= tol) {
+        *converged = 1;
+        break;
+      }
+    }
+  });
+}
+
 // fine_periodicity_defect (proj/src/engine.cpp:272-290)
 // Diagnostic: time one PCG phase of the last nonlinear propagation's batch as a
 // standalone kernel (see phase_probe_kernel).  mode 0 = phase A (TMA-staged),

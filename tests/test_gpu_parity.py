@@ -352,3 +352,14 @@ def test_pp_ic_nonlinear_radial_cable_matches_oracle():
     assert rel_l2(res.trajectory, U_o) <= TOL
     pc = ps.solve_pp_pc(cable, ps.EngineSettings(mesh, tol=1e-8, max_iterations=10))
     assert pc.history["iterations"] < res.history["iterations"]
+
+
+def test_sequential_steady_state_matches_oracle():
+    """§8(f) rank 4: proj/src/propagators.cpp:117-149 on the device (batch size 1)."""
+    for prob, mesh, tol in ((ps.build_dae_pair(), None, 1e-9), (ps.build_coax_cable(n_r=41), None, 1e-8)):
+        mesh = ps.TimeMesh(8, 5, prob.period) if prob.dim == 2 else ps.TimeMesh(4, 10, prob.period)
+        res = ps.sequential_steady_state(prob, mesh, tol, 5000)
+        S, per, conv, defs = po.Oracle(prob).sequential_steady_state(mesh, tol, 5000, mode=po.ITERATIVE)
+        assert res.converged and conv and res.periods == per
+        assert rel_l2(res.trajectory, S) <= TOL
+        assert abs(res.period_defects[-1] - defs[-1]) <= 1e-6 * max(defs[-1], 1e-300) + 1e-15
