@@ -342,6 +342,29 @@ void ps_problem_free(ps_problem* p);
 /* Error message of the last failed builder call on this thread. */
 const char* ps_builder_error(void);
 /* Seeded N(0, sigma^2) samples: std::mt19937_64(seed) + explicit Box-Muller. */
+/* Files (host C++, no device work).
+ * Matrix Market [proj/src/matrix_market.cpp:30-93]: coordinate real general or
+ * symmetric storage, duplicates summed; written in column-major entry order with
+ * shortest round-trip values.  Errors: ps_builder_error(). */
+typedef struct ps_csr ps_csr;
+int ps_mm_read(const char* path, ps_csr** out);
+int ps_csr_shape(const ps_csr* m, int32_t* rows, int32_t* cols, int64_t* nnz);
+const int32_t* ps_csr_row_ptr(const ps_csr* m);
+const int32_t* ps_csr_col_idx(const ps_csr* m);
+const double* ps_csr_values(const ps_csr* m);
+void ps_csr_free(ps_csr* m);
+int ps_mm_write(const char* path, int32_t rows, int32_t cols, const int32_t* row_ptr, const int32_t* col_idx,
+                const double* values);
+/* load_problem [proj/src/problem.cpp:363-421]: linear problem from M, K Matrix
+ * Market files and the excitation JSON (parse_excitation_text's schema). */
+int ps_load_problem(const char* mass_path, const char* stiffness_path, const char* excitation_path,
+                    ps_problem** out);
+/* format_double, write_trajectory_csv, write_history_csv [proj/src/io.cpp:151-178] */
+int ps_format_double(double value, char* buf, int32_t len);
+int ps_write_trajectory_csv(const char* path, int32_t count, int32_t dim, const double* states,
+                            const ps_time_mesh* mesh);
+int ps_write_history_csv(const char* path, int32_t count, const double* jumps, const double* seconds);
+
 void ps_seeded_normal(uint64_t seed, int64_t count, double sigma, double* out);
 /* Seeded U(lo, hi) samples: mt19937_64 53-bit mantissa mapping. */
 void ps_seeded_uniform(uint64_t seed, int64_t count, double lo, double hi, double* out);

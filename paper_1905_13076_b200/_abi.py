@@ -159,6 +159,17 @@ _SIGNATURES = {
     "ps_problem_coordinates": (dp, [vp]),
     "ps_problem_free": (None, [vp]),
     "ps_builder_error": (C.c_char_p, []),
+    "ps_mm_read": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "ps_csr_shape": (C.c_int, [vp, ip, ip, C.POINTER(C.c_int64)]),
+    "ps_csr_row_ptr": (ip, [vp]),
+    "ps_csr_col_idx": (ip, [vp]),
+    "ps_csr_values": (dp, [vp]),
+    "ps_csr_free": (None, [vp]),
+    "ps_mm_write": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, ip, ip, dp]),
+    "ps_load_problem": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(vp)]),
+    "ps_format_double": (C.c_int, [C.c_double, C.c_char_p, C.c_int32]),
+    "ps_write_trajectory_csv": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, dp, C.POINTER(ps_time_mesh)]),
+    "ps_write_history_csv": (C.c_int, [C.c_char_p, C.c_int32, dp, dp]),
     "ps_seeded_normal": (None, [C.c_uint64, C.c_int64, C.c_double, dp]),
     "ps_seeded_uniform": (None, [C.c_uint64, C.c_int64, C.c_double, C.c_double, dp]),
 }

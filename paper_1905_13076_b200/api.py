@@ -319,6 +319,78 @@ def build_dae_pair() -> PeriodicProblem:
                                   [dict(pattern=[1.0, 0.0], amplitude=1.0, frequency=50.0)], 1.0 / 50.0)
 
 
+# --------------------------------------------------------------------- files
+def _builder_fail(rc):
+    raise ParasteadyError(rc, lib().ps_builder_error().decode())
+
+
+def read_matrix_market(path: str):
+    """proj/src/matrix_market.cpp:30-81 -> scipy.sparse.csr_matrix."""
+    import scipy.sparse as sp
+    h = C.c_void_p()
+    rc = lib().ps_mm_read(str(path).encode(), C.byref(h))
+    if rc != _abi.PS_OK:
+        _builder_fail(rc)
+    try:
+        r, c, n = C.c_int32(0), C.c_int32(0), C.c_int64(0)
+        lib().ps_csr_shape(h, C.byref(r), C.byref(c), C.byref(n))
+        rp = np.ctypeslib.as_array(lib().ps_csr_row_ptr(h), shape=(r.value + 1,)).copy()
+        ci = np.ctypeslib.as_array(lib().ps_csr_col_idx(h), shape=(max(1, n.value),))[:n.value].copy()
+        va = np.ctypeslib.as_array(lib().ps_csr_values(h), shape=(max(1, n.value),))[:n.value].copy()
+        return sp.csr_matrix((va, ci, rp), shape=(r.value, c.value))
+    finally:
+        lib().ps_csr_free(h)
+
+
+def write_matrix_market(path: str, matrix) -> None:
+    """proj/src/matrix_market.cpp:83-93 (general storage, shortest round-trip values)."""
+    import scipy.sparse as sp
+    m = sp.csr_matrix(matrix)
+    m.sort_indices()
+    rp = np.ascontiguousarray(m.indptr, dtype=np.int32)
+    ci = np.ascontiguousarray(m.indices, dtype=np.int32)
+    va = _f64(m.data)
+    rc = lib().ps_mm_write(str(path).encode(), m.shape[0], m.shape[1], _ip(rp), _ip(ci), _dp(va))
+    if rc != _abi.PS_OK:
+        _builder_fail(rc)
+
+
+def load_problem(mass_path: str, stiffness_path: str, excitation_path: str) -> PeriodicProblem:
+    """proj/src/problem.cpp:363-421: the "files" problem class on the device path."""
+    h = C.c_void_p()
+    rc = lib().ps_load_problem(str(mass_path).encode(), str(stiffness_path).encode(), str(excitation_path).encode(),
+                               C.byref(h))
+    if rc != _abi.PS_OK:
+        _builder_fail(rc)
+    return PeriodicProblem._from_builder(h)
+
+
+def format_double(value: float) -> str:
+    """proj/src/io.cpp:151-155 (shortest round-trip decimal)."""
+    buf = C.create_string_buffer(64)
+    _raise(lib().ps_format_double(float(value), buf, 64))
+    return buf.value.decode()
+
+
+def write_trajectory_csv(path: str, states, mesh: TimeMesh) -> None:
+    """proj/src/io.cpp:157-170."""
+    S = _f64(states)
+    if S.ndim == 1:
+        S = S.reshape(-1, 1)
+    rc = lib().ps_write_trajectory_csv(str(path).encode(), S.shape[0], S.shape[1], _dp(S), C.byref(mesh.c()))
+    if rc != _abi.PS_OK:
+        _builder_fail(rc)
+
+
+def write_history_csv(path: str, jumps, seconds=None) -> None:
+    """proj/src/io.cpp:172-178."""
+    j = _f64(jumps).reshape(-1)
+    s = None if seconds is None else _f64(seconds).reshape(-1)
+    rc = lib().ps_write_history_csv(str(path).encode(), j.shape[0], _dp(j), _dp(s))
+    if rc != _abi.PS_OK:
+        _builder_fail(rc)
+
+
 def seeded_normal(seed: int, count: int, sigma: float) -> np.ndarray:
     out = np.empty(count, dtype=np.float64)
     lib().ps_seeded_normal(seed, count, sigma, _dp(out))

@@ -363,3 +363,23 @@ def test_sequential_steady_state_matches_oracle():
         assert res.converged and conv and res.periods == per
         assert rel_l2(res.trajectory, S) <= TOL
         assert abs(res.period_defects[-1] - defs[-1]) <= 1e-6 * max(defs[-1], 1e-300) + 1e-15
+
+
+def test_files_problem_runs_the_device_path(tmp_path):
+    """§8(f) rank 2: the reference's "files" problem class (Matrix Market M, K +
+    excitation JSON, proj/src/problem.cpp:363-421) through PP-PC on the device
+    gives the built-in DAE pair's result bit for bit."""
+    ref = ps.build_dae_pair()
+    ps.write_matrix_market(str(tmp_path / "m.mtx"), ref.csr(ref.mass_values))
+    ps.write_matrix_market(str(tmp_path / "k.mtx"), ref.csr(ref.stiffness_values))
+    (tmp_path / "f.json").write_text('{"period": 0.02, "terms": [{"amplitude": 1.0, "frequency": 50.0, '
+                                     '"dofs": [0], "values": [1.0]}]}')
+    loaded = ps.load_problem(str(tmp_path / "m.mtx"), str(tmp_path / "k.mtx"), str(tmp_path / "f.json"))
+    es = ps.EngineSettings(ps.TimeMesh(8, 5, ref.period), tol=1e-10)
+    a = ps.solve_pp_pc(ref, es)
+    b = ps.solve_pp_pc(loaded, es)
+    assert a.history["iterations"] == b.history["iterations"]
+    assert np.array_equal(a.trajectory, b.trajectory)
+    ps.write_trajectory_csv(str(tmp_path / "trajectory.csv"), b.trajectory, es.mesh)
+    rows = (tmp_path / "trajectory.csv").read_text().splitlines()
+    assert len(rows) == 9 and float(rows[1].split(",")[2]) == b.trajectory[0, 0]
