@@ -291,9 +291,9 @@ int ps_sequential_steady_state(ps_ctx* ctx, double tol, int32_t max_periods, dou
                                int32_t* periods, int32_t* converged, double* defects);
 
 /* Diagnostics: time one PCG phase of the last nonlinear propagation's batch as a
- * standalone (ncu-replayable) kernel: mode 0 = SpMV phase (TMA-staged rows),
- * 1 = SpMV phase (register pipeline), 2 = update phase.  bytes_out = the phase's
- * DRAM bytes by the SURVEY.md §8d stream count. */
+ * standalone (ncu-replayable) kernel: mode 1 = SpMV phase, 2 = update phase,
+ * 3 = the update phase's streams as a flat copy.  bytes_out = the phase's bytes
+ * by the SURVEY.md §8d stream count. */
 int ps_phase_probe(ps_ctx* ctx, int32_t mode, int32_t reps, double* ms_out, double* bytes_out);
 
 /* --------------------------------------------------------------- builders */

@@ -1620,11 +1620,10 @@ int ps_sequential_steady_state(ps_ctx* ctx, double tol, int32_t max_periods, dou
   });
 }
 
-// fine_periodicity_defect (proj/src/engine.cpp:272-290)
 // Diagnostic: time one PCG phase of the last nonlinear propagation's batch as a
-// standalone kernel (see phase_probe_kernel).  mode 0 = phase A (TMA-staged),
-// 1 = phase A (register pipeline), 2 = phase B.  ms_out = mean over reps;
-// bytes_out = the phase's DRAM bytes by the SURVEY.md §8d stream count.
+// standalone kernel (see phase_probe_kernel).  mode 1 = phase A (SpMV + dots),
+// 2 = phase B (updates), 3 = phase B's streams as a flat copy.  ms_out = mean
+// over reps; bytes_out = the phase's bytes by the SURVEY.md §8d stream count.
 int ps_phase_probe(ps_ctx* ctx, int32_t mode, int32_t reps, double* ms_out, double* bytes_out) {
   if (!ctx || reps < 1) return PS_ERR_BAD_ARG;
   std::lock_guard<std::mutex> lock(ctx->mu);
@@ -1647,6 +1646,7 @@ int ps_phase_probe(ps_ctx* ctx, int32_t mode, int32_t reps, double* ms_out, doub
   });
 }
 
+// fine_periodicity_defect (proj/src/engine.cpp:272-290)
 int ps_fine_periodicity_defect(ps_ctx* ctx, const double* U, double* defect) {
   if (!ctx || !U || !defect) return PS_ERR_BAD_ARG;
   const int N = ctx->mesh.subintervals, d = ctx->P.d;
