@@ -908,6 +908,16 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         acc[0] += isfinite(xs[iv]) ? 0.0 : 1.0;
       }
     }
+    // hub row operands for the phase-A transition, loaded before the barrier so
+    // their latency overlaps it
+    double hub_p = 0.0, hub_r = 0.0, hub_d = 0.0;
+    if (warp == 0 && act == ACT_A && P.hub_split) {
+      const int hub = __ldg(P.long_rows);
+      const size_t ih = static_cast<size_t>(gs) * P.d * kLanes + sl + static_cast<size_t>(hub) * kLanes;
+      hub_p = P.p[ih];
+      hub_r = P.r[ih];
+      hub_d = row_shared(P, hub) ? __ldg(P.Dsh + hub) : P.Dinv[ih];
+    }
     {
       const SyncCtx X{P.sync, P.partials, P.abort_flag, P.G, P.C, 32, P.L};
       if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, P.dbg ? &t_arr : nullptr)) {
@@ -927,7 +937,9 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
       Lane& s = lanes[lane];
       int a = act;
       int stp = step;
-      const double t_now = (a != ACT_IDLE) ? P.t_next[static_cast<size_t>(stp) * P.count + sys] : 0.0;
+      // the step's time is only needed to report a failure: read it then, not on
+      // every interval's critical path
+      auto t_now_of = [&]() { return P.t_next[static_cast<size_t>(stp) * P.count + sys]; };
       double t0v = sh.tot[0][sl], t1v = sh.tot[1][sl], t2v = sh.tot[2][sl];
       const double t3v = sh.tot[3][sl];
       if (a == ACT_A && P.hub_split) {
@@ -936,8 +948,8 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         // stores it for phase B
         const int hub = __ldg(P.long_rows);
         const size_t ih = static_cast<size_t>(gs) * P.d * kLanes + sl + static_cast<size_t>(hub) * kLanes;
-        const double qh = t3v, ph = P.p[ih], rh = P.r[ih];
-        const double dh = row_shared(P, hub) ? __ldg(P.Dsh + hub) : P.Dinv[ih];
+        const double qh = t3v, ph = hub_p, rh = hub_r;
+        const double dh = hub_d;
         t0v += ph * qh;
         t1v += qh * (dh * rh);
         t2v += qh * (dh * qh);
@@ -958,7 +970,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         }
         case ACT_A: {
           if (!isfinite(t0v) || t0v == 0.0) {
-            lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
+            lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now_of());
           } else {
             s.alpha = s.rho / t0v;
             const double rho_est = s.rho - 2.0 * s.alpha * t1v + s.alpha * s.alpha * t2v;
@@ -977,9 +989,9 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
             s.max_pit = max(s.max_pit, s.pit);
             a = LINEAR ? ACT_LU : ACT_U;
           } else if (!isfinite(rr)) {
-            lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now);
+            lane_fail(s, PS_ERR_SINGULAR, LINEAR ? 0.0 : s.res_pre, t_now_of());
           } else if (s.pit >= P.pcg_max) {
-            lane_fail(s, PS_ERR_PCG_MAXITER, LINEAR ? 0.0 : s.res_pre, t_now);
+            lane_fail(s, PS_ERR_PCG_MAXITER, LINEAR ? 0.0 : s.res_pre, t_now_of());
           } else {
             a = ACT_A;
           }
@@ -987,7 +999,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         }
         case ACT_U: {
           if (!s.bt && t0v > 0.0)
-            lane_fail(s, PS_ERR_SINGULAR, s.res_pre, t_now);
+            lane_fail(s, PS_ERR_SINGULAR, s.res_pre, t_now_of());
           else
             a = ACT_R;
           break;
@@ -1005,7 +1017,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
           s.bt = false;
           if (writer && P.trace) P.trace[static_cast<size_t>(sys) * P.newton_max + (s.nit - 1)] = post;
           if (!isfinite(post)) {
-            lane_fail(s, PS_ERR_NEWTON_DIVERGED, post, t_now);
+            lane_fail(s, PS_ERR_NEWTON_DIVERGED, post, t_now_of());
           } else if (post <= s.tol) {
             s.newton_total += s.nit;
             s.last_nit = s.nit;
@@ -1013,7 +1025,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
             ++stp;
             a = stp < P.steps ? ACT_R0 : ACT_IDLE;
           } else if (s.nit >= P.newton_max) {
-            lane_fail(s, PS_ERR_NEWTON_MAXITER, post, t_now);
+            lane_fail(s, PS_ERR_NEWTON_MAXITER, post, t_now_of());
           } else {
             s.nit += 1;
             s.res_pre = post;
@@ -1032,7 +1044,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         }
         case ACT_LU: {
           if (t0v > 0.0) {
-            lane_fail(s, PS_ERR_SINGULAR, 0.0, t_now);
+            lane_fail(s, PS_ERR_SINGULAR, 0.0, t_now_of());
           } else {
             s.newton_total += 1;
             s.last_nit = 1;
