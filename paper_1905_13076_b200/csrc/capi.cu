@@ -400,7 +400,12 @@ Geometry& geometry(ps_ctx* ctx, int count) {
   g.Lp = 32;
   g.R = 1;
   const int g_max = sequential_groups() ? 1 : (ctx->max_batch + 31) / 32;
-  const int rows_min = kWarps * 4;
+  // at least rows_min rows per block: two rows per warp.  Small problems then
+  // spread over more SMs (configs[0], d = 2,497: 79 blocks, fine sweep 969 ->
+  // 832 ms against four rows per warp; one row per warp is slower again, the
+  // barrier then dominates).  PPPC_ROWS_MIN overrides (diagnostics).
+  static const int rows_min = std::getenv("PPPC_ROWS_MIN") ? std::max(1, std::atoi(std::getenv("PPPC_ROWS_MIN")))
+                                                           : kWarps * 2;
   if (g_max > ctx->capacity) throw Failure(PS_ERR_BAD_ARG, "propagator: batch too large for one cooperative launch");
   g.C = std::max(1, std::min(ctx->capacity / g_max, (ctx->P.d + rows_min - 1) / rows_min));
   std::vector<int> ranges;
