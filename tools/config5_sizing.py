@@ -1,0 +1,84 @@
+#!/usr/bin/env python3
+"""BASELINE configs[4] sizing sweep (measurement, bounded): the saturation-stress
+cable (Brauer k2 = 4.0, I0 = 8000 A) on the nr = 2000 x ntheta = 2048 mesh
+(d = 4,093,953), N in {16, 64, 256} subintervals batched on one GPU.
+
+The full workload (10 fine steps to PCG 1e-12 at this size) takes hours. This tool
+measures what the sweep is about: that every N fits in HBM, and the device throughput
+at that size. Per N it reports:
+  * peak device memory after the context and the batch are resident;
+  * one Newton iteration of the first fine step for all N systems (PCG relaxed to
+    --pcg-tol, Newton capped at one iteration, so the lanes stop with "Newton did not
+    converge", which is expected here): time, PCG counts, algorithmic GB/s;
+  * the standalone phase probes (SpMV and update phase) at this size.
+Start states are N(0, 1e-3), generated on the device (torch, seeded).
+
+  python tools/config5_sizing.py [--N 16 64 256] [--pcg-tol 1e-6]
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_1905_13076_b200 as ps  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--N", type=int, nargs="*", default=[16, 64, 256])
+ap.add_argument("--nr", type=int, default=2000)
+ap.add_argument("--ntheta", type=int, default=2048)
+ap.add_argument("--pcg-tol", type=float, default=1e-2)
+a = ap.parse_args()
+
+t0 = time.perf_counter()
+prob = ps.build_polar_cable(nr=a.nr, ntheta=a.ntheta, brauer_k2=4.0, current=8000.0)
+build_s = time.perf_counter() - t0
+d = prob.dim
+dev = torch.device("cuda", 0)
+peak = 6530.3
+try:
+    peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+except Exception:
+    pass
+for N in a.N:
+    torch.cuda.synchronize()
+    mesh = ps.TimeMesh(N, 10, prob.period)
+    newton = ps.NewtonSettings(tol_abs=1e-6, tol_rel=1e-10, max_iter=1, line_search=0)
+    prop = ps.Propagator(prob, ps.TimeMesh(N * 10, 1, prob.period), newton,
+                         ps.KrylovSettings(tol_rel=a.pcg_tol, max_iter=5000), max_batch=N)
+    g = torch.Generator(device=dev)
+    g.manual_seed(19051307 + N)
+    U = torch.randn((N, d), generator=g, device=dev, dtype=torch.float64) * 1e-3
+    out = torch.empty_like(U)
+    t1 = time.perf_counter()
+    try:
+        prop.fine_propagate_batch_dev(1, N, U.data_ptr(), out.data_ptr())
+    except ps.ParasteadyError as exc:  # one Newton iteration by design
+        print(f"N={N}: {exc}", file=sys.stderr, flush=True)
+    st = prop.last_status
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t1
+    free, total = torch.cuda.mem_get_info(dev)
+    probes = {}
+    for mode in (1, 2):
+        ms, by = C.c_double(0), C.c_double(0)
+        prop._check(ps.lib().ps_phase_probe(prop._ctx, mode, 3, C.byref(ms), C.byref(by)))
+        probes[f"mode{mode}"] = {"us": ms.value * 1e3, "GBps": by.value / (ms.value / 1e3) / 1e9,
+                                 "frac": by.value / (ms.value / 1e3) / 1e9 / peak}
+    line = {"measurement": "BASELINE configs[4] sizing (bounded: one Newton iteration of one step, PCG relaxed)",
+            "nr": a.nr, "ntheta": a.ntheta, "dof": d, "nnz": prob.nnz, "N": N, "build_s": build_s,
+            "device_used_GB": (total - free) / 1e9, "device_total_GB": total / 1e9,
+            "step_wall_s": wall, "kernel_ms": st.kernel_ms, "newton_iterations": st.newton_iterations,
+            "pcg_iterations": st.pcg_iterations, "pcg_tol": a.pcg_tol,
+            "algorithmic_GBps": st.algorithmic_bytes / (st.kernel_ms / 1e3) / 1e9,
+            "frac": st.algorithmic_bytes / (st.kernel_ms / 1e3) / 1e9 / peak, "phase_probes": probes,
+            "status": st.code}
+    print(json.dumps(line), flush=True)
+    prop.close()
+    del U, out
+    torch.cuda.empty_cache()
