@@ -65,7 +65,7 @@ for N in a.N:
     wall = time.perf_counter() - t1
     free, total = torch.cuda.mem_get_info(dev)
     probes = {}
-    for mode in (1, 2):
+    for mode in (1, 2, 3):
         ms, by = C.c_double(0), C.c_double(0)
         prop._check(ps.lib().ps_phase_probe(prop._ctx, mode, 3, C.byref(ms), C.byref(by)))
         probes[f"mode{mode}"] = {"us": ms.value * 1e3, "GBps": by.value / (ms.value / 1e3) / 1e9,
