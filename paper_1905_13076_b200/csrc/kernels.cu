@@ -230,25 +230,27 @@ __device__ __forceinline__ void refill_row_ell(const PropParams& P, const ps_cur
   const int base = h.x, len = h.y;
   const bool shared_row = P.rowkind == nullptr || h.z == 0;
   const int c[kEll] = {c03.x, c03.y, c03.z, c03.w, c47.x, c47.y, c47.z, c47.w};
-  // the row's u entries go to the lane's scratch column right away (few
-  // registers held), the mass term is formed as soon as u_prev arrives
+  // the row's u and u_prev entries and padded mass row are all issued in one
+  // round (one memory latency per row instead of three); u then goes to the
+  // lane's scratch column
+  const double* me = P.ME + static_cast<size_t>(i) * kEll;
+  double mr = 0.0;
   {
-    double uc[kEll];
+    double uc[kEll], upc[kEll], mv[kEll];
 #pragma unroll
     for (int k = 0; k < kEll; ++k) uc[k] = P.u[vo + static_cast<size_t>(c[k]) * kLanes];
 #pragma unroll
+    for (int k = 0; k < kEll; ++k) upc[k] = first ? 0.0 : P.uprev[vo + static_cast<size_t>(c[k]) * kLanes];
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) mv[k] = __ldg(me + k);
+#pragma unroll
     for (int k = 0; k < kEll; ++k) us[k][lane] = uc[k];
-  }
-  const double* me = P.ME + static_cast<size_t>(i) * kEll;
-  double mr = 0.0;
-  if (!first) {
-    double upc[kEll];
-#pragma unroll
-    for (int k = 0; k < kEll; ++k) upc[k] = P.uprev[vo + static_cast<size_t>(c[k]) * kLanes];
     // mass term M (u - u_prev)/dt, zero at the first Newton iterate of a step
+    if (!first) {
 #pragma unroll
-    for (int k = 0; k < kEll; ++k)
-      if (k < len) mr += __ldg(me + k) * ((us[k][lane] - upc[k]) / P.dt);
+      for (int k = 0; k < kEll; ++k)
+        if (k < len) mr += mv[k] * ((uc[k] - upc[k]) / P.dt);
+    }
   }
   double ku = 0.0;
   if (shared_row) {
