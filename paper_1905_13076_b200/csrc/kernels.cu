@@ -230,6 +230,22 @@ __device__ __forceinline__ void refill_row_ell(const PropParams& P, const ps_cur
   const int base = h.x, len = h.y;
   const bool shared_row = P.rowkind == nullptr || h.z == 0;
   const int c[kEll] = {c03.x, c03.y, c03.z, c03.w, c47.x, c47.y, c47.z, c47.w};
+  // the operands of the row's later rounds (shared stiffness row, excitation
+  // coefficients and patterns, Jacobi entry, element adjacency) are requested
+  // into L1 now, so those rounds hit L1 instead of waiting on L2
+  {
+    const char* ke = reinterpret_cast<const char*>(P.KE + static_cast<size_t>(i) * kEll);
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(ke));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(ke + 32));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms));
+    for (int t = 0; t < P.nterms; ++t)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P.pat + static_cast<size_t>(t) * P.d + i));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.Dsh + i));
+    if (!shared_row) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P.adj_ptr + i));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P.adj + __ldg(P.adj_ptr + i)));
+    }
+  }
   // the row's u and u_prev entries and padded mass row are all issued in one
   // round (one memory latency per row instead of three); u then goes to the
   // lane's scratch column
