@@ -672,10 +672,13 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
         wmin = std::min(wmin, w);
         wmax = std::max(wmax, w);
       }
+      double rel = 0;
+      for (int b = 0; b < nblk; ++b) rel += static_cast<double>(h[b * W + 18 + kind]);
       if (n > 0)
         std::fprintf(stderr,
-                     "[pppc timing] %s: %.0f intervals/block, work %.2f us (block min %.2f max %.2f), wait %.2f us\n",
-                     names[kind], n / nblk, work / n / 1e3, wmin / 1e3, wmax / 1e3, wait / n / 1e3);
+                     "[pppc timing] %s: %.0f intervals/block, work %.2f us (block min %.2f max %.2f), wait %.2f us "
+                     "(arrival -> release seen %.2f us)\n",
+                     names[kind], n / nblk, work / n / 1e3, wmin / 1e3, wmax / 1e3, wait / n / 1e3, rel / n / 1e3);
       if (std::getenv("PPPC_DEBUG_BLOCKS")) {
         std::fprintf(stderr, "[pppc blocks %s]", names[kind]);
         for (int b = 0; b < nblk; ++b) {

@@ -106,6 +106,7 @@ __device__ bool group_sync_reduce(const SyncCtx& X, SyncShared<NDMAX>& sh, doubl
       __nanosleep(20);
     }
     __threadfence();
+    if (t_arrive) t_arrive[1] = globaltimer_ns();  // release seen (diagnostics)
     sh.abort = ab;
     sh.bar_idx += 1;
   }

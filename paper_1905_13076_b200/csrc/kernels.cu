@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
   // Loop-carried state is kept minimal (barrier state and counters in shared
   // memory, addresses recomputed per interval from g, c, warp, lane) so the
   // phase pipelines get the registers.
-  __shared__ unsigned long long t_start, t_arr;  // debug timing (thread 0)
+  __shared__ unsigned long long t_start, t_arr[2];  // debug timing (thread 0): arrival, release seen
   // optional per-block timing (P.dbg): work / barrier-wait ns and counts for
   // intervals where lane 0 ran phase A, phase B, or anything else
   // plus per-action lane-interval counts (dbg[9 + action])
@@ -938,7 +938,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     }
     {
       const SyncCtx X{P.sync, P.partials, P.abort_flag, P.G, P.C, 32, P.L};
-      if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, P.dbg ? &t_arr : nullptr)) {
+      if (!group_sync_reduce<kNDots, 4>(X, sh, acc, g, c, P.dbg ? t_arr : nullptr)) {
         aborted = true;
         return false;
       }
@@ -946,9 +946,10 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     if (P.dbg && warp == 0 && valid) atomicAdd(&dbg[9 + act], 1ull);
     if (P.dbg && threadIdx.x == 0) {
       const unsigned long long t_end = globaltimer_ns();
-      dbg[3 * dbg_kind + 0] += t_arr - t_start;
-      dbg[3 * dbg_kind + 1] += t_end - t_arr;
+      dbg[3 * dbg_kind + 0] += t_arr[0] - t_start;
+      dbg[3 * dbg_kind + 1] += t_end - t_arr[0];
       dbg[3 * dbg_kind + 2] += 1;
+      dbg[18 + dbg_kind] += t_arr[1] - t_arr[0];
     }
     // ------------------------------------------------ transitions (warp 0)
     if (warp == 0) {

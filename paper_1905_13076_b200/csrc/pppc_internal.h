@@ -17,7 +17,7 @@ constexpr int kThreads = kWarps * 32;  // 512
 constexpr int kMaxCurves = 8;
 constexpr int kMaxTerms = 16;
 constexpr int kNDots = 4;
-constexpr int kDbgSlots = 18;          // debug timing: 9 timing words + 9 action counts
+constexpr int kDbgSlots = 21;          // debug timing: 9 timing words + 9 action counts + 3 release times
 constexpr int kRegularRow = 7;         // rows with <= 7 slots (the P1 polar mesh) use register accumulators
 constexpr int kLongRow = 32;           // rows with > 32 slots are split across a block's warps
 // Row records: rowrec[3i] = {first slot, length, kind (1 = per-system values),
