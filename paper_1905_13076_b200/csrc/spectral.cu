@@ -205,18 +205,34 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
       __syncthreads();
     }
     if (s.act && row_begin + sub < row_end) {
-      // row records one row ahead of their use
+      // row records two rows ahead of their use; the next row's gathered p
+      // entries, own p / r and slot values are requested into L1 one row ahead
+      // (no registers held), so the row's loads mostly hit L1
       int i = row_begin + sub;
       int4 h0 = __ldg(P.rowrec + kRecInts4 * i), c03 = __ldg(P.rowrec + kRecInts4 * i + 1),
            c47 = __ldg(P.rowrec + kRecInts4 * i + 2);
+      int4 h1 = h0, d03 = c03, d47 = c47;
+      if (i + P.R < row_end) {
+        h1 = __ldg(P.rowrec + kRecInts4 * (i + P.R));
+        d03 = __ldg(P.rowrec + kRecInts4 * (i + P.R) + 1);
+        d47 = __ldg(P.rowrec + kRecInts4 * (i + P.R) + 2);
+      }
       for (;;) {
-        const int i1 = i + P.R;
+        const int i1 = i + P.R, i2 = i + 2 * P.R;
         const bool more = i1 < row_end;
-        int4 h1 = h0, d03 = c03, d47 = c47;
-        if (more) {
-          h1 = __ldg(P.rowrec + kRecInts4 * i1);
-          d03 = __ldg(P.rowrec + kRecInts4 * i1 + 1);
-          d47 = __ldg(P.rowrec + kRecInts4 * i1 + 2);
+        int4 h2 = h1, e03 = d03, e47 = d47;
+        if (i2 < row_end) {
+          h2 = __ldg(P.rowrec + kRecInts4 * i2);
+          e03 = __ldg(P.rowrec + kRecInts4 * i2 + 1);
+          e47 = __ldg(P.rowrec + kRecInts4 * i2 + 2);
+        }
+        if (more && h1.y <= kEll) {
+          const int cn[kEll] = {d03.x, d03.y, d03.z, d03.w, d47.x, d47.y, d47.z, d47.w};
+#pragma unroll
+          for (int k = 0; k < kEll; ++k)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(P.p + static_cast<size_t>(cn[k]) * H + h));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(P.r + static_cast<size_t>(i1) * H + h));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(P.XYE + static_cast<size_t>(i1) * kEll));
         }
         const int len = h0.y;
         if (len <= kEll) {
@@ -247,6 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
         h0 = h1;
         c03 = d03;
         c47 = d47;
+        h1 = h2;
+        d03 = e03;
+        d47 = e47;
       }
     }
     if (!group_sync_reduce<kCND, 6>(X, sh, acc, g, c)) return;
