@@ -308,6 +308,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "frac_vs_nominal_8000": achieved / 8000.0,
                      "dram_gbs_measured": (traffic / (kernel_ms / 1e3) / 1e9) if traffic else None,
                      "kernel": "propagate_kernel<false,3> (persistent Newton + Jacobi-PCG)",
                      "peak_source": peak_src,
