@@ -22,6 +22,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -42,7 +44,6 @@ def parse():
     ap.add_argument("--subintervals", type=int, default=100)
     ap.add_argument("--fine-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-steps", type=int, default=4)
     ap.add_argument("--cpu-sample-systems", type=int, default=0)
     ap.add_argument("--pcg-tol", type=float, default=1e-12,
                     help="profiling runs only: a looser PCG tolerance shortens the kernel under ncu replay")
@@ -55,7 +56,7 @@ def workload(args):
     import paper_1905_13076_b200 as ps
     prob = ps.build_polar_cable(nr=args.nr, ntheta=args.ntheta)
     mesh = ps.TimeMesh(args.subintervals, args.fine_steps, prob.period)
-    newton = ps.NewtonSettings(tol_abs=1e-6, tol_rel=1e-10, max_iter=50, line_search=30)
+    newton = ps.NewtonSettings(tol_abs=1e-9, tol_rel=1e-10, max_iter=50, line_search=30)
     pcg = ps.KrylovSettings(tol_rel=args.pcg_tol, max_iter=50000)
     return prob, mesh, newton, pcg
 
@@ -69,13 +70,25 @@ def start_states(prob, n_sub, rank):
     return U
 
 
+def max_over_ranks_of(x, world, device):
+    """Max of a per-rank scalar (the device time of the timed region) over all
+    ranks; device = the rank's CUDA device under NCCL, cpu under gloo."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def config_dict(args, prob):
     return {
         "workload": "BASELINE configs[1]: batched fine propagators, 2-D polar P1 cable",
         "nr": args.nr, "ntheta": args.ntheta, "dof": prob.dim, "nnz": prob.nnz,
-        "subintervals_per_gpu": args.subintervals, "fine_steps": args.fine_steps,
+        "subintervals": args.subintervals, "fine_steps": args.fine_steps,
         "current_A": 2000.0, "start_values": "N(0, 1e-3) per DOF, seeded",
-        "newton": "tol_rel 1e-10, tol_abs 1e-6, max 50, backtracking 30 (DESIGN.md §2)",
+        "newton": "tol_rel 1e-10, tol_abs 1e-9, max 50, backtracking 30 (DESIGN.md §2)",
         "pcg": "Jacobi, rel 1e-12", "l2": "inputs larger than L2 (states + per-system matrices > 126 MB)",
     }
 
@@ -152,59 +165,155 @@ def ncu_traffic(args):
         return None
 
 
-def cpu_baseline(args, prob, mesh, newton, pcg, U, steps_sample=None, systems=None):
-    """The oracle (reference algorithm restated: Newton with a fresh sparse LDL^T per
-    iteration, proj/src/propagators.cpp:27-58) on all host cores, bounded sample."""
-    import numpy as np
-    import paper_1905_13076_b200 as ps
+def oracle_native():
+    """Load the CPU oracle rebuilt with -march=native for the host it runs on (the
+    in-tree liboracle_pppc.so is built portable in the container).  Only the CPU
+    timing legs use this copy; it is the same source, oracle/oracle.cpp +
+    oracle/polar_mesh.cpp.  Falls back to the portable build if the compile fails."""
+    import importlib
+    lib_dir = os.path.join(ROOT, "oracle", "_native")
+    os.makedirs(lib_dir, exist_ok=True)
+    path = os.path.join(lib_dir, "liboracle_native.so")
+    srcs = [os.path.join(ROOT, "oracle", f) for f in ("oracle.cpp", "polar_mesh.cpp")]
+    try:
+        subprocess.run(["/usr/bin/g++", "-O3", "-march=native", "-ffp-contract=off", "-std=c++17", "-fPIC",
+                        "-pthread", "-shared", *srcs, "-o", path], check=True, capture_output=True, timeout=300)
+        os.environ["PPPC_ORACLE_LIB"] = path
+    except Exception:
+        pass
     from oracle import pyoracle as po
-    cores = os.cpu_count() or 1
-    steps_sample = steps_sample or args.cpu_sample_steps
-    systems = systems or args.cpu_sample_systems or min(args.subintervals, cores)
-    sub_mesh = ps.TimeMesh(mesh.subintervals, steps_sample, mesh.period)
-    # same step length as the full workload: dt = T/(N s); sample = first `steps_sample`
-    # steps of `systems` subintervals (mesh with s' steps keeps dt only if s' == s), so
-    # run the full-s mesh but limit time by stepping the first steps via newton_step
+    return importlib.reload(po)
+
+
+def reference_problem(args):
+    """configs[1] built by the ORACLE's own builder and generators (never the
+    product library): the same bits the product builder produces
+    (tests/test_builders.py::test_oracle_builder_is_bit_identical)."""
+    po = oracle_native()
+    prob = po.build_polar_cable(nr=args.nr, ntheta=args.ntheta)
+    from paper_1905_13076_b200.api import KrylovSettings, NewtonSettings, TimeMesh
+    mesh = TimeMesh(args.subintervals, args.fine_steps, prob.period)
+    newton = NewtonSettings(tol_abs=1e-9, tol_rel=1e-10, max_iter=50, line_search=30)
+    pcg = KrylovSettings(tol_rel=args.pcg_tol, max_iter=50000)
+    U = np.empty((args.subintervals, prob.dim))
+    for n in range(1, args.subintervals + 1):
+        U[n - 1] = po.seeded_normal(SEED + n, prob.dim, 1e-3)
+    return po, prob, mesh, newton, pcg, U
+
+
+class CpuSampler:
+    """Bounded samples of the configs[1] workload on the host cores, by the
+    reference's algorithm: implicit Euler with Newton and a fresh sparse LDL^T per
+    iteration (proj/src/propagators.cpp:27-58), the subintervals of a batch in
+    parallel, one per core (proj/src/engine.cpp:226-227).
+
+    advance() runs ONE fine step of `systems` consecutive subintervals and keeps
+    their states, so s consecutive calls propagate those subintervals over all
+    their fine steps exactly as the full workload does: the first, expensive
+    steps from the random start and the cheap later ones are sampled in their
+    true proportion.  After the last fine step the sampler moves on to the next
+    `systems` subintervals."""
+
+    def __init__(self, po, orc, mesh, newton, pcg, U, systems):
+        import concurrent.futures as cf
+        self.po, self.orc, self.mesh, self.newton, self.pcg, self.U = po, orc, mesh, newton, pcg, U
+        self.systems = systems
+        self.pool = cf.ThreadPoolExecutor(max_workers=systems)
+        self.block = 0
+        self.j = 0
+        self.newton_iterations = 0
+        self.system_steps = 0
+        self._start_block()
+
+    def _start_block(self):
+        N = self.mesh.subintervals
+        self.n_first = 1 + (self.block * self.systems) % max(1, N - self.systems + 1)
+        self.state = [self.U[self.n_first - 1 + i].copy() for i in range(self.systems)]
+        self.j = 0
+
+    def advance(self):
+        m, dt = self.mesh, self.mesh.fine_dt()
+        j = self.j + 1
+
+        def one(i):
+            n = self.n_first + i
+            # TimeMesh: t_j = T_{n-1} + j dt, the last step lands on T_n exactly
+            t_next = m.boundary(n) if j == m.fine_steps else m.boundary(n - 1) + j * dt
+            u, its, _, _ = self.orc.newton_step(self.state[i], t_next, dt, newton=self.newton, pcg=self.pcg,
+                                                mode=self.po.DIRECT)
+            self.state[i] = u
+            return its
+
+        t0 = time.perf_counter()
+        its = list(self.pool.map(one, range(self.systems)))
+        el = time.perf_counter() - t0
+        self.newton_iterations += sum(its)
+        self.system_steps += self.systems
+        self.j = j
+        if j == m.fine_steps:
+            self.block += 1
+            self._start_block()
+        return el, self.systems * self.orc.dim
+
+
+def cpu_baseline(args):
+    """The reference algorithm on the host cores over a bounded sample (SURVEY.md
+    §8d): `cores` subintervals x all s fine steps."""
+    po, prob, mesh, newton, pcg, U = reference_problem(args)
     orc = po.Oracle(prob)
-    dt = mesh.fine_dt()
-    t0 = time.perf_counter()
-    import concurrent.futures as cf
-
-    def one(n):
-        u = U[n].copy()
-        t_left = mesh.boundary(n)
-        for j in range(1, steps_sample + 1):
-            t_next = mesh.boundary(n + 1) if j == mesh.fine_steps else t_left + j * dt
-            u, _, _, _ = orc.newton_step(u, t_next, dt, newton=newton, pcg=pcg, mode=po.DIRECT)
-        return u
-
-    with cf.ThreadPoolExecutor(max_workers=cores) as ex:
-        list(ex.map(one, range(systems)))
-    el = time.perf_counter() - t0
-    del sub_mesh
-    value = systems * steps_sample * prob.dim / el
-    return {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{systems} subintervals x first {steps_sample} fine step(s) of the config, direct LDL^T "
-                      f"Newton (reference algorithm), {cores} threads, {el:.1f} s"}
+    cores = os.cpu_count() or 1
+    systems = min(args.subintervals, args.cpu_sample_systems or cores)
+    smp = CpuSampler(po, orc, mesh, newton, pcg, U, systems)
+    el = units = 0.0
+    for _ in range(mesh.fine_steps):
+        e, u = smp.advance()
+        el += e
+        units += u
+    return {"value": units / el, "unit": UNIT, "cores": systems, "kind": "port",
+            "sample": f"subintervals 1..{systems} x all {mesh.fine_steps} fine steps (the full trajectories of "
+                      f"{systems} of the {mesh.subintervals} subintervals), direct LDL^T Newton (reference "
+                      f"algorithm, oracle built -march=native), {systems} threads, {el:.1f} s",
+            "newton_per_system_step": smp.newton_iterations / smp.system_steps}
 
 
 def run_reference(args):
+    """bench.py --impl reference: the reference's CPU algorithm (the oracle port;
+    the reference itself cannot be built here) on the host cores.
+    Problem and start values come from the oracle's own builder and generators,
+    so this process never loads libpppc_b200.so.  Each timed step is one fine
+    step of `cores` subintervals (CpuSampler), consecutive steps continuing the
+    same trajectories; warm-up steps propagate one subinterval by one fine step
+    (a CPU code has nothing to warm beyond page-in)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    prob, mesh, newton, pcg = workload(args)
-    U = start_states(prob, args.subintervals, 0)
-    vals = []
-    for k in range(args.warmup + args.steps):
-        cb = cpu_baseline(args, prob, mesh, newton, pcg, U)
-        if k >= args.warmup:
-            vals.append(cb["value"])
-    value = statistics.median(vals)
-    cb["value"] = value
+    po, prob, mesh, newton, pcg, U = reference_problem(args)
+    orc = po.Oracle(prob)
+    cores = os.cpu_count() or 1
+    systems = min(args.subintervals, args.cpu_sample_systems or cores)
+    for _ in range(args.warmup):
+        orc.newton_step(U[0], mesh.boundary(0) + mesh.fine_dt(), mesh.fine_dt(), newton=newton, pcg=pcg,
+                        mode=po.DIRECT)
+    smp = CpuSampler(po, orc, mesh, newton, pcg, U, systems)
+    el = units = 0.0
+    for _ in range(args.steps):
+        e, u = smp.advance()
+        el += e
+        units += u
+    value = units / el
+    maps = open("/proc/self/maps").read()
+    cb = {"value": value, "unit": UNIT, "cores": systems, "kind": "port",
+          "sample": f"per step: one fine step of {systems} subintervals (one per core), consecutive steps "
+                    f"continuing the same trajectories ({args.steps} steps = {args.steps / mesh.fine_steps:.2f} "
+                    f"x the s = {mesh.fine_steps} steps of a subinterval); direct LDL^T Newton (reference "
+                    f"algorithm, oracle built -march=native); {el:.1f} s",
+          "newton_per_system_step": smp.newton_iterations / smp.system_steps,
+          "product_library_loaded": "libpppc_b200" in maps}
+    cfg = config_dict(args, prob)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": args.subintervals * args.fine_steps * prob.dim / value * 1e3,
+            "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_dict(args, prob), "impl": "reference",
+            "data": "synthetic", "config": cfg, "impl": "reference",
             "cpu_baseline": cb, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -242,11 +351,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return max_over_ranks_of(x, world, dev)
 
     # warm-up (device-resident inputs)
     for _ in range(args.warmup):
@@ -299,7 +404,8 @@ def run_ours(args):
     last = statuses[-1]
     traffic = ncu_traffic(args)
     cfg = config_dict(args, prob)
-    cfg["parallelism"] = f"{world} GPU(s) x {N} subintervals each (independent fine propagators)"
+    if world > 1:
+        cfg["parallelism"] = f"{world} GPU(s) x {N} subintervals each (independent fine propagators)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -319,9 +425,10 @@ def run_ours(args):
                    "max_newton_per_step": last["max_newton_iterations"]},
         "clocks": clk.summary(),
     }
+    line["solver"]["newton_per_system_step"] = last["newton_iterations"] / (N * s)
     if world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline(args, prob, mesh, newton, pcg, U_host)
+            line["cpu_baseline"] = cpu_baseline(args)
         except Exception as exc:  # the baseline must never hide the GPU number
             line["cpu_baseline"] = {"value": None, "error": str(exc)}
     print(json.dumps(line), flush=True)

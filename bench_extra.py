@@ -19,7 +19,7 @@ import numpy as np  # noqa: E402
 
 import paper_1905_13076_b200 as ps  # noqa: E402
 
-NEWTON = ps.NewtonSettings(tol_abs=1e-6, tol_rel=1e-10, max_iter=50, line_search=30)
+NEWTON = ps.NewtonSettings(tol_abs=1e-9, tol_rel=1e-10, max_iter=50, line_search=30)
 
 
 def peak():

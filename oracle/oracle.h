@@ -99,6 +99,19 @@ int or_sequential_steady_state(const or_problem* p, const ps_time_mesh* mesh,
                                int32_t max_periods, double* U_out, int32_t* periods,
                                int32_t* converged, double* defects);
 
+/* The oracle's own builders and seeded generators (polar_mesh.cpp): the canonical
+ * polar P1 cable of SURVEY.md App. A.1 and the SURVEY.md §8(d) generators,
+ * independent of the product library's builders. */
+typedef struct or_mesh or_mesh;
+int or_polar_cable_defaults(ps_polar_cable_params* p);
+int or_build_polar_cable(const ps_polar_cable_params* params, or_mesh** out);
+const char* or_mesh_error(void);
+const ps_problem_desc* or_mesh_desc(const or_mesh* m);
+const double* or_mesh_coordinates(const or_mesh* m);
+void or_mesh_free(or_mesh* m);
+void or_seeded_normal(uint64_t seed, int64_t count, double sigma, double* out);
+void or_seeded_uniform(uint64_t seed, int64_t count, double lo, double hi, double* out);
+
 #ifdef __cplusplus
 }
 #endif

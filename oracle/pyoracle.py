@@ -1,8 +1,12 @@
 """ctypes wrapper of liboracle_pppc.so — TEST INFRASTRUCTURE ONLY.
 
 The oracle is the CPU restatement of the reference algorithm (oracle.cpp).  It
-consumes the same ps_problem_desc as the device library, so tests and the
-bench hand both sides identical inputs."""
+consumes a ps_problem_desc: either its own (build_polar_cable / seeded_normal
+below come from oracle/polar_mesh.cpp, so the reference arm of bench.py never
+loads the product library) or the product builder's, which tests/test_builders.py
+proves bit-identical.  Only the ctypes declarations and plain settings
+dataclasses are shared with the product package; nothing here loads
+libpppc_b200.so."""
 from __future__ import annotations
 
 import ctypes as C
@@ -15,7 +19,8 @@ from paper_1905_13076_b200.api import (EngineSettings, KrylovSettings, NewtonSet
                                        TimeMesh, solver_settings)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(HERE, "liboracle_pppc.so")
+# PPPC_ORACLE_LIB: the same source built for the host (bench.py oracle_native)
+LIB = os.environ.get("PPPC_ORACLE_LIB") or os.path.join(HERE, "liboracle_pppc.so")
 DIRECT, ITERATIVE = 0, 1
 
 dp, ip, vp = _abi.dp, _abi.ip, C.c_void_p
@@ -67,6 +72,14 @@ _SIG = {
                                  C.POINTER(_abi.ps_history), C.c_int32]),
     "or_fine_periodicity_defect": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh),
                                              C.POINTER(_abi.ps_solver_settings), C.c_int32, dp, dp, C.c_int32]),
+    "or_polar_cable_defaults": (C.c_int, [C.POINTER(_abi.ps_polar_cable_params)]),
+    "or_build_polar_cable": (C.c_int, [C.POINTER(_abi.ps_polar_cable_params), C.POINTER(vp)]),
+    "or_mesh_error": (C.c_char_p, []),
+    "or_mesh_desc": (C.POINTER(_abi.ps_problem_desc), [vp]),
+    "or_mesh_coordinates": (dp, [vp]),
+    "or_mesh_free": (None, [vp]),
+    "or_seeded_normal": (None, [C.c_uint64, C.c_int64, C.c_double, dp]),
+    "or_seeded_uniform": (None, [C.c_uint64, C.c_int64, C.c_double, C.c_double, dp]),
     "or_sequential_steady_state": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh),
                                              C.POINTER(_abi.ps_solver_settings), C.c_int32, C.c_double,
                                              C.c_int32, dp, ip, ip, dp]),
@@ -102,6 +115,63 @@ def _check(rc):
 
 def workers_default():
     return max(1, os.cpu_count() or 1)
+
+
+class OracleProblem:
+    """A problem built by the oracle's own builder (oracle/polar_mesh.cpp): the
+    same accessors Oracle needs (desc, coordinates) plus numpy views."""
+
+    def __init__(self, handle):
+        self._h = handle
+        self.desc = lib().or_mesh_desc(handle).contents
+        self.dim, self.nnz = int(self.desc.dim), int(self.desc.nnz)
+        self.period = float(self.desc.period)
+        self.coordinates = np.ctypeslib.as_array(lib().or_mesh_coordinates(handle), shape=(self.dim, 2)).copy()
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().or_mesh_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def array(self, name):
+        d = self.desc
+        n = {"row_ptr": self.dim + 1, "col_idx": self.nnz, "mass": self.nnz, "stiffness": self.nnz,
+             "elem_nodes": d.n_elem * d.nodes_per_elem, "elem_stiff": d.n_elem * d.nodes_per_elem ** 2,
+             "elem_inv_area": d.n_elem, "elem_curve": d.n_elem, "patterns": d.n_terms * self.dim,
+             "amplitude": d.n_terms, "frequency_hz": d.n_terms, "phase_rad": d.n_terms}[name]
+        ptr = getattr(d, name)
+        if not ptr:
+            return None
+        return np.ctypeslib.as_array(ptr, shape=(n,)).copy()
+
+
+def build_polar_cable(**params) -> OracleProblem:
+    """The canonical polar P1 cable from the oracle's own builder."""
+    p = _abi.ps_polar_cable_params()
+    lib().or_polar_cable_defaults(C.byref(p))
+    for k, v in params.items():
+        if not hasattr(p, k):
+            raise ParasteadyError(_abi.PS_ERR_BAD_ARG, f"problem: unknown polar cable parameter {k!r}")
+        setattr(p, k, v)
+    h = vp()
+    if lib().or_build_polar_cable(C.byref(p), C.byref(h)) != 0:
+        raise ParasteadyError(_abi.PS_ERR_BAD_ARG, lib().or_mesh_error().decode())
+    return OracleProblem(h)
+
+
+def seeded_normal(seed: int, count: int, sigma: float) -> np.ndarray:
+    out = np.empty(count)
+    lib().or_seeded_normal(seed, count, sigma, _p(out))
+    return out
+
+
+def seeded_uniform(seed: int, count: int, lo: float, hi: float) -> np.ndarray:
+    out = np.empty(count)
+    lib().or_seeded_uniform(seed, count, lo, hi, _p(out))
+    return out
 
 
 class Oracle:

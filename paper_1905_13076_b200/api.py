@@ -545,7 +545,7 @@ class Propagator:
 
     # -- spectral (linear contexts)
     def mh_setup(self, use_conjugate_symmetry=True, bin_mask=None, shift_kind=0):
-        mask = None if bin_mask is None else np.ascontiguousarray(bin_mask, dtype=np.int32)
+        mask = _checked_mask(bin_mask, self.mesh.subintervals, use_conjugate_symmetry)
         self._mask = mask
         self._check(lib().ps_mh_setup(self._ctx, int(bool(use_conjugate_symmetry)), _ip(mask), int(shift_kind)))
 
@@ -679,6 +679,29 @@ def assemble_rhs(fine, coarse, linear: Propagator) -> np.ndarray:
 
 
 # -------------------------------------------------------------------- engine
+def _checked_mask(bin_mask, n_blocks: int, use_conjugate_symmetry: bool):
+    """The C ABI reads bins 0..N/2 (conjugate symmetry) or 0..N-1 of the mask."""
+    if bin_mask is None:
+        return None
+    mask = np.ascontiguousarray(bin_mask, dtype=np.int32).reshape(-1)
+    need = n_blocks // 2 + 1 if use_conjugate_symmetry else n_blocks
+    if mask.shape[0] != need:
+        raise ParasteadyError(_abi.PS_ERR_BAD_ARG, f"spectral: bin mask needs {need} entries, got {mask.shape[0]}")
+    return mask
+
+
+def _checked_reference(ref, dim: int):
+    """frozen_coarse_linearization (proj/src/engine.cpp:66-74): empty = zero state."""
+    if ref is None:
+        return None
+    ref = _f64(ref).reshape(-1)
+    if ref.shape[0] == 0:
+        return None
+    if ref.shape[0] != dim:
+        raise ParasteadyError(_abi.PS_ERR_BAD_ARG, "engine: frozen reference state dimension mismatch")
+    return ref
+
+
 @dataclass
 class PeriodicSolveResult:
     trajectory: np.ndarray          # [N][d] states at T_0..T_{N-1}
@@ -697,10 +720,10 @@ def solve_pp_pc(problem: PeriodicProblem, settings: EngineSettings, keep_iterate
         e.tol = settings.tol
         e.max_iterations = settings.max_iterations
         e.use_conjugate_symmetry = int(bool(settings.use_conjugate_symmetry))
-        mask = None if settings.bin_mask is None else np.ascontiguousarray(settings.bin_mask, dtype=np.int32)
+        mask = _checked_mask(settings.bin_mask, mesh.subintervals, settings.use_conjugate_symmetry)
         e.bin_mask = _ip(mask)
         e.shift_kind = settings.shift_kind
-        ref = None if settings.frozen_reference is None else _f64(settings.frozen_reference)
+        ref = _checked_reference(settings.frozen_reference, problem.dim)
         U = np.empty((mesh.subintervals, problem.dim))
         its = (np.empty((settings.max_iterations, mesh.subintervals, problem.dim)) if keep_iterates else None)
         h = _abi.ps_history()

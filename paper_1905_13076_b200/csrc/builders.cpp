@@ -410,13 +410,13 @@ int ps_build_polar_cable(const ps_polar_cable_params* params, ps_problem** out) 
       }
     pr.build_pattern();
 
-    // consistent P1 conductivity mass sigma A/12 [[2,1,1],[1,2,1],[1,1,2]]
+    // consistent P1 conductivity mass sigma A/12 [[2,1,1],[1,2,1],[1,1,2]]; the
+    // source patterns are uniform current densities whose P1 loads A/3 on the
+    // free nodes are normalised so the conductor carries exactly +1 and the
+    // sheath returns exactly -1 (the Dirichlet ring takes no share)
     const double region_sigma[3] = {P.sigma_conductor, P.sigma_insulator, P.sigma_sheath};
-    double region_area[3] = {0.0, 0.0, 0.0};
-    for (int64_t e = 0; e < n_elem; ++e) region_area[region[e]] += area[e];
-    std::vector<double> pattern(pr.dim, 0.0);
-    const double j_cond = 1.0 / region_area[0];
-    const double j_sheath = P.return_in_sheath ? -1.0 / region_area[2] : 0.0;
+    std::vector<double> load_c(pr.dim, 0.0), load_s(pr.dim, 0.0);
+    double sum_c = 0.0, sum_s = 0.0;
     for (int64_t e = 0; e < n_elem; ++e) {
       const double s = region_sigma[region[e]];
       const int32_t* nd = &pr.elem_nodes[e * 3];
@@ -430,12 +430,20 @@ int ps_build_polar_cable(const ps_polar_cable_params* params, ps_problem** out) 
           }
         }
       }
-      const double jd = region[e] == 0 ? j_cond : (region[e] == 2 ? j_sheath : 0.0);
-      if (jd != 0.0) {
-        const double load = jd * area[e] / 3.0;
-        for (int a = 0; a < 3; ++a)
-          if (nd[a] >= 0) pattern[nd[a]] += load;
-      }
+      if (region[e] == 1) continue;
+      const double w = area[e] / 3.0;
+      std::vector<double>& load = region[e] == 0 ? load_c : load_s;
+      double& sum = region[e] == 0 ? sum_c : sum_s;
+      for (int a = 0; a < 3; ++a)
+        if (nd[a] >= 0) {
+          load[nd[a]] += w;
+          sum += w;
+        }
+    }
+    std::vector<double> pattern(pr.dim, 0.0);
+    for (int i = 0; i < pr.dim; ++i) {
+      pattern[i] = load_c[i] / sum_c;
+      if (P.return_in_sheath) pattern[i] -= load_s[i] / sum_s;
     }
 
     // excitation: I0 sin(2 pi f t) plus an optional odd-harmonic square ripple

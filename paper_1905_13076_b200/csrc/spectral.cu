@@ -411,8 +411,9 @@ __global__ void dft_forward_kernel(int d, int N, int H, const int* __restrict__ 
 // owns sample n = t mod N for rows t / N, t / N + k, ... of every tile it
 // visits, so its partial sums run in a fixed order; part[block][2][N].
 __global__ void idft_jump_kernel(int d, int N, int H, const int* __restrict__ bins, const double2* __restrict__ tw,
-                                 int conj, const double2* __restrict__ xhat, double* __restrict__ U,
-                                 const double* __restrict__ U_old, double* part, double* maxre, double* maxim) {
+                                 int conj, const double2* __restrict__ xhat, double* U, const double* U_old,
+                                 double* part, double* maxre, double* maxim) {
+  // U and U_old may alias (in-place PP-PC correction): no __restrict__ on them
   extern __shared__ double2 ism[];
   double2* stw = ism;                                         // [N]
   double2* sx = ism + N;                                      // [kDftRows][H]
@@ -622,6 +623,17 @@ int dalloc(T** p, size_t n) {
 
 }  // namespace
 
+// dynamic shared memory of the two spectral tile kernels (spectral_solve)
+size_t dft_forward_smem(int N, int H) {
+  return static_cast<size_t>(N) * sizeof(double2) + static_cast<size_t>(kDftRows) * N * sizeof(double) +
+         static_cast<size_t>(H) * sizeof(int);
+}
+int idft_threads(int N) { return N * std::max(1, 512 / N); }  // thread t owns sample t mod N
+size_t idft_smem(int N, int H) {
+  return static_cast<size_t>(N) * sizeof(double2) + static_cast<size_t>(kDftRows) * H * sizeof(double2) +
+         static_cast<size_t>(2) * idft_threads(N) * sizeof(double) + static_cast<size_t>(H) * sizeof(int);
+}
+
 struct SpectralState {
   int N = 0, d = 0, nnz = 0, H = 0;
   double period = 0.0;
@@ -823,11 +835,26 @@ int spectral_setup(SpectralState** out, const DevProblem& p, int N, double perio
     }
   }
   cudaMemcpy(s->coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice);
-  // spectral tiles: up to 1024 samples and 513 bins in dynamic shared memory
-  cudaFuncSetAttribute(reinterpret_cast<const void*>(dft_forward_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       160 * 1024);
-  cudaFuncSetAttribute(reinterpret_cast<const void*>(idft_jump_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       160 * 1024);
+  // spectral tiles: opt in to the device's shared-memory maximum and reject a
+  // (N, bins) combination whose tiles do not fit (e.g. N = 1024 with
+  // use_conjugate_symmetry = 0 asks for ~164 KB in the inverse tile)
+  {
+    int dev = 0, smax = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t need = std::max(dft_forward_smem(N, s->H), idft_smem(N, s->H));
+    if (need > static_cast<size_t>(smax)) {
+      *err = "spectral: " + std::to_string(N) + " blocks with " + std::to_string(s->H) +
+             " solved bins need " + std::to_string(need) + " bytes of shared memory per spectral tile (device max " +
+             std::to_string(smax) + ")";
+      spectral_free(s);
+      return PS_ERR_BAD_ARG;
+    }
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(dft_forward_kernel),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(idft_jump_kernel),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+  }
   cudaEventCreate(&s->e0);
   cudaEventCreate(&s->e1);
   if (rc != PS_OK || cudaGetLastError() != cudaSuccess) {
@@ -868,12 +895,12 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
   int64_t lock_total = 0, its_total = 0;
   int max_its = 0;
   if (H > 0) {
-    const int64_t tot = static_cast<int64_t>(d) * H;
-    const size_t fsm = static_cast<size_t>(N) * sizeof(double2) + static_cast<size_t>(kDftRows) * N * sizeof(double) +
-                       static_cast<size_t>(H) * sizeof(int);
     const int ftpb = std::min(1024, ((kDftRows * H + 31) / 32) * 32);
-    dft_forward_kernel<<<s->idft_blocks, ftpb, fsm, st>>>(d, N, H, s->d_bins, s->tw, rhs, s->bhat);
-    (void)tot;
+    dft_forward_kernel<<<s->idft_blocks, ftpb, dft_forward_smem(N, H), st>>>(d, N, H, s->d_bins, s->tw, rhs, s->bhat);
+    if (const cudaError_t le = cudaGetLastError(); le != cudaSuccess) {
+      *err = std::string("cuda: dft_forward launch failed: ") + cudaGetErrorString(le);
+      return PS_ERR_CUDA;
+    }
     cudaMemsetAsync(s->sync, 0, s->G * sizeof(unsigned long long), st);
     cudaMemsetAsync(s->abort_flag, 0, sizeof(int), st);
     CocgParams P{};
@@ -918,12 +945,17 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
       return PS_ERR_CUDA;
     }
   }
-  const int tpb = N * std::max(1, 512 / N);  // thread t owns sample t mod N
-  const size_t smem = static_cast<size_t>(N) * sizeof(double2) + static_cast<size_t>(kDftRows) * H * sizeof(double2) +
-                      static_cast<size_t>(2) * tpb * sizeof(double) + static_cast<size_t>(H) * sizeof(int);
-  idft_jump_kernel<<<s->idft_blocks, tpb, smem, st>>>(d, N, H, s->d_bins, s->tw, s->conj, s->x, U_il, U_prev_il,
-                                                      s->jpart, s->maxre, s->maxim);
+  idft_jump_kernel<<<s->idft_blocks, idft_threads(N), idft_smem(N, H), st>>>(
+      d, N, H, s->d_bins, s->tw, s->conj, s->x, U_il, U_prev_il, s->jpart, s->maxre, s->maxim);
+  if (const cudaError_t le = cudaGetLastError(); le != cudaSuccess) {
+    *err = std::string("cuda: idft_jump launch failed: ") + cudaGetErrorString(le);
+    return PS_ERR_CUDA;
+  }
   jump_finalize_kernel<<<1, 1024, 0, st>>>(N, s->idft_blocks, s->idft_blocks, s->jpart, s->maxre, s->maxim, s->jout);
+  if (const cudaError_t le = cudaGetLastError(); le != cudaSuccess) {
+    *err = std::string("cuda: jump_finalize launch failed: ") + cudaGetErrorString(le);
+    return PS_ERR_CUDA;
+  }
   cudaEventRecord(s->e1, st);
   double hj[5];
   cudaMemcpyAsync(hj, s->jout, sizeof(hj), cudaMemcpyDeviceToHost, st);

@@ -28,12 +28,12 @@ def test_polar_invariants():
     assert np.max(np.abs(K0 - K0.T)) <= 1e-12 * np.max(np.abs(K0))
     assert np.min(np.linalg.eigvalsh(K0)) > 0.0
     pat = p.excitation_terms()[0]["pattern"]
-    # conductor carries exactly +1 (no Dirichlet node inside r < 2 mm); the sheath
-    # return is -1 minus the share of the Dirichlet ring
+    # the conductor carries exactly +1 and the sheath returns exactly -1 over the
+    # free DOFs (proj/tests/test_problem.cpp:128-135 invariant)
     r = np.hypot(*p.coordinates.T)
-    assert abs(pat[r < 2e-3 + 1e-9].sum() - 1.0) <= 1e-12
-    sheath = pat[r > 4e-3 - 1e-9].sum()
-    assert -1.0 < sheath < -0.5
+    assert abs(pat[r < 2e-3 + 1e-9].sum() - 1.0) <= 1e-13
+    assert abs(pat[r > 4e-3 - 1e-9].sum() + 1.0) <= 1e-13
+    assert abs(pat.sum()) <= 1e-13
     # J - K is PSD (element weights 2 B^2 nu' >= 0), proj/tests/test_problem.cpp:165-172
     u = np.linspace(0, 5e-3, p.dim)
     orc = po.Oracle(p)
@@ -124,3 +124,41 @@ def test_excitation_frequency_validation_matches_reference():
     bad = ps.PeriodicProblem.linear([[1.0]], [[1.0]], [dict(pattern=[1.0], amplitude=1.0, frequency=75.0)], 0.02)
     with pytest.raises(ps.ParasteadyError, match="integer multiple"):
         po.Oracle(bad)
+
+
+@pytest.mark.parametrize("kw", [dict(nr=2, ntheta=4), dict(nr=10, ntheta=16), dict(),
+                                dict(nr=12, ntheta=16, ripple_terms=5), dict(nr=40, ntheta=64, linear_sheath=1),
+                                dict(nr=200, ntheta=256), dict(nr=33, ntheta=7, return_in_sheath=0, current=20.0)])
+def test_oracle_builder_is_bit_identical(kw):
+    """The oracle's own polar builder (oracle/polar_mesh.cpp) and the product
+    builder (csrc/builders.cpp) are written independently; every array of the
+    problem description they hand to the two sides must agree bit for bit, so
+    feeding the oracle either problem is the same check (VERDICT r1 weak #4)."""
+    a = ps.build_polar_cable(**kw)
+    b = po.build_polar_cable(**kw)
+    assert (a.dim, a.nnz, a.period) == (b.dim, b.nnz, b.period)
+    da, db = a.desc, b.desc
+    for f in ("n_elem", "nodes_per_elem", "n_curves", "n_terms"):
+        assert getattr(da, f) == getattr(db, f), f
+    for k in range(da.n_curves):
+        ca, cb = da.curves[k], db.curves[k]
+        assert (ca.kind, ca.nu, ca.k1, ca.k2, ca.k3) == (cb.kind, cb.nu, cb.k1, cb.k2, cb.k3)
+    n = dict(row_ptr=a.dim + 1, col_idx=a.nnz, mass=a.nnz, stiffness=a.nnz,
+             elem_nodes=da.n_elem * 3, elem_stiff=da.n_elem * 9, elem_inv_area=da.n_elem,
+             elem_curve=da.n_elem, patterns=da.n_terms * a.dim, amplitude=da.n_terms,
+             frequency_hz=da.n_terms, phase_rad=da.n_terms)
+    for name, cnt in n.items():
+        pa, pb = getattr(da, name), getattr(db, name)
+        assert bool(pa) == bool(pb), name
+        if not pa:
+            continue
+        xa = np.ctypeslib.as_array(pa, shape=(cnt,))
+        xb = np.ctypeslib.as_array(pb, shape=(cnt,))
+        assert xa.tobytes() == xb.tobytes(), name
+    assert a.coordinates.tobytes() == b.coordinates.tobytes()
+
+
+def test_oracle_generators_are_bit_identical():
+    for seed, n in ((19051307, 1), (19051308, 50945), (5, 7)):
+        assert ps.seeded_normal(seed, n, 1e-3).tobytes() == po.seeded_normal(seed, n, 1e-3).tobytes()
+        assert ps.seeded_uniform(seed, n, 0.5, 1.5).tobytes() == po.seeded_uniform(seed, n, 0.5, 1.5).tobytes()

@@ -276,7 +276,7 @@ def test_line_search_extension_rescues_deep_saturation():
     mesh = ps.TimeMesh(100, 20, prob.period)
     orc = po.Oracle(prob)
     u0 = ps.seeded_normal(19051308, prob.dim, 1e-3).reshape(1, -1)
-    plain = ps.NewtonSettings(tol_abs=1e-6, tol_rel=1e-10, max_iter=50)
+    plain = ps.NewtonSettings(tol_abs=1e-9, tol_rel=1e-10, max_iter=50)
     with pytest.raises(ps.ParasteadyError, match="Newton did not converge"):
         orc.fine_propagate_batch(mesh, 1, u0, newton=plain, mode=po.DIRECT)
     F = orc.fine_propagate_batch(mesh, 1, u0, newton=NEWTON_BASELINE, mode=po.DIRECT)

@@ -48,7 +48,7 @@ except Exception:
 for N in a.N:
     torch.cuda.synchronize()
     mesh = ps.TimeMesh(N, 10, prob.period)
-    newton = ps.NewtonSettings(tol_abs=1e-6, tol_rel=1e-10, max_iter=1, line_search=0)
+    newton = ps.NewtonSettings(tol_abs=1e-9, tol_rel=1e-10, max_iter=1, line_search=0)
     prop = ps.Propagator(prob, ps.TimeMesh(N * 10, 1, prob.period), newton,
                          ps.KrylovSettings(tol_rel=a.pcg_tol, max_iter=5000), max_batch=N)
     g = torch.Generator(device=dev)
