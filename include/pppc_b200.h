@@ -296,6 +296,25 @@ int ps_sequential_steady_state(ps_ctx* ctx, double tol, int32_t max_periods, dou
  * by the SURVEY.md §8d stream count. */
 int ps_phase_probe(ps_ctx* ctx, int32_t mode, int32_t reps, double* ms_out, double* bytes_out);
 
+/* Test probes of the hot-path kernels themselves (not of a whole solve).
+ * ps_refill_probe: one fused refill (refill_row_ell / refill_long_rows /
+ *   refill_finish inside the persistent propagation kernel) of `count` systems
+ *   at (U, U_prev, t_next, dt): A = M/dt + J(U) [count][nnz], R = M (U - U_prev)/dt
+ *   + K(U) U - f(t_next) [count][dim], Dinv = 1/diag(A) [count][dim]; any output
+ *   may be NULL [proj/src/propagators.cpp:13-17, proj/src/problem.cpp:344-359].
+ * ps_mh_bins: the solved bins of the context's spectral setup (returns their
+ *   count, or minus an error code).
+ * ps_mh_forward: dft_forward_kernel, rhs [N][dim] -> spectrum [H][dim] complex
+ *   (re, im pairs) on the solved bins [proj/src/spectral.cpp:32-63].
+ * ps_mh_inverse: idft_jump_kernel + jump_finalize_kernel, spectrum [H][dim] ->
+ *   mirrored, realified U [N][dim] and jump_norm against U_old (or NULL)
+ *   [proj/src/spectral.cpp:72-84,270-278, proj/src/engine.cpp:54-64]. */
+int ps_refill_probe(ps_ctx* ctx, int32_t count, const double* U, const double* U_prev,
+                    const double* t_next, double dt, double* A_out, double* R_out, double* Dinv_out);
+int ps_mh_bins(ps_ctx* ctx, int32_t* bins, int32_t cap);
+int ps_mh_forward(ps_ctx* ctx, const double* rhs, double* spectrum);
+int ps_mh_inverse(ps_ctx* ctx, const double* spectrum, const double* U_old, double* U, double* jump);
+
 /* --------------------------------------------------------------- builders */
 typedef struct ps_problem ps_problem;
 /* 2-D structured polar P1 cable (BASELINE.json configs). */

@@ -220,8 +220,8 @@ int or_build_polar_cable(const ps_polar_cable_params* prm, or_mesh** out) {
     // DOFs: the conductor carries +1 and the sheath returns exactly -1
     std::vector<double> pattern(dim);
     for (int i = 0; i < dim; ++i) {
-      pattern[i] = load_c[i] / sum_c;
-      if (P.return_in_sheath) pattern[i] -= load_s[i] / sum_s;
+      pattern[i] = sum_c > 0.0 ? load_c[i] / sum_c : 0.0;
+      if (P.return_in_sheath && sum_s > 0.0) pattern[i] -= load_s[i] / sum_s;
     }
     m->pat = pattern;
     m->amp = {P.current};

@@ -196,4 +196,8 @@ def lib() -> C.CDLL:
     return _lib
 
 _SIGNATURES["ps_phase_probe"] = (C.c_int, [vp, C.c_int32, C.c_int32, dp, dp])
+_SIGNATURES["ps_refill_probe"] = (C.c_int, [vp, C.c_int32, dp, dp, dp, C.c_double, dp, dp, dp])
+_SIGNATURES["ps_mh_bins"] = (C.c_int, [vp, ip, C.c_int32])
+_SIGNATURES["ps_mh_forward"] = (C.c_int, [vp, dp, dp])
+_SIGNATURES["ps_mh_inverse"] = (C.c_int, [vp, dp, dp, dp, dp])
 EXPORTED = sorted(_SIGNATURES)

@@ -565,6 +565,45 @@ class Propagator:
         self._check(rc)
         return out
 
+    # -- kernel probes (tests of the hot-path kernels themselves)
+    def refill_probe(self, U, U_prev, t_next, dt: float):
+        """One fused refill inside the persistent kernel: (A = M/dt + J(U) [n][nnz],
+        R = M (U - U_prev)/dt + K(U) U - f(t_next) [n][d], Dinv [n][d])."""
+        U = self._states(U)
+        Up = self._states(U_prev, U.shape[0])
+        t = _f64(np.broadcast_to(np.asarray(t_next, dtype=np.float64), (U.shape[0],)))
+        A = np.empty((U.shape[0], self.problem.nnz))
+        R = np.empty_like(U)
+        D = np.empty_like(U)
+        self._check(lib().ps_refill_probe(self._ctx, U.shape[0], _dp(U), _dp(Up), _dp(t), float(dt), _dp(A), _dp(R),
+                                          _dp(D)))
+        return A, R, D
+
+    def mh_bins(self):
+        buf = np.zeros(self.mesh.subintervals + 1, dtype=np.int32)
+        n = lib().ps_mh_bins(self._ctx, _ip(buf), buf.shape[0])
+        if n < 0:
+            self._check(-n)
+        return buf[:n].copy()
+
+    def mh_forward(self, rhs) -> np.ndarray:
+        """dft_forward_kernel on the solved bins: [H][d] complex."""
+        R = self._states(rhs, self.mesh.subintervals)
+        H = len(self.mh_bins())
+        out = np.empty((H, self.dim, 2))
+        self._check(lib().ps_mh_forward(self._ctx, _dp(R), _dp(out)))
+        return out[..., 0] + 1j * out[..., 1]
+
+    def mh_inverse(self, spectrum, U_old=None):
+        """idft_jump_kernel + jump_finalize_kernel: (U [N][d], jump)."""
+        S = np.asarray(spectrum, dtype=np.complex128)
+        buf = np.ascontiguousarray(np.stack([S.real, S.imag], axis=-1))
+        old = None if U_old is None else self._states(U_old, self.mesh.subintervals)
+        U = np.empty((self.mesh.subintervals, self.dim))
+        jump = C.c_double(0.0)
+        self._check(lib().ps_mh_inverse(self._ctx, _dp(buf), _dp(old), _dp(U), C.byref(jump)))
+        return U, jump.value
+
     def pppc_correct(self, F, G, U):
         F = self._states(F, self.mesh.subintervals)
         G = self._states(G, self.mesh.subintervals)

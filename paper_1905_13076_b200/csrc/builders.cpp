@@ -442,8 +442,9 @@ int ps_build_polar_cable(const ps_polar_cable_params* params, ps_problem** out) 
     }
     std::vector<double> pattern(pr.dim, 0.0);
     for (int i = 0; i < pr.dim; ++i) {
-      pattern[i] = load_c[i] / sum_c;
-      if (P.return_in_sheath) pattern[i] -= load_s[i] / sum_s;
+      // (a region without elements carries no source)
+      pattern[i] = sum_c > 0.0 ? load_c[i] / sum_c : 0.0;
+      if (P.return_in_sheath && sum_s > 0.0) pattern[i] -= load_s[i] / sum_s;
     }
 
     // excitation: I0 sin(2 pi f t) plus an optional odd-harmonic square ripple

@@ -478,7 +478,7 @@ struct PropResult {
 // [steps][count].  newton_mode: run Newton even for linear problems
 // (newton_step semantics) instead of the linear fast path.
 PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::vector<double>& t_next,
-                     bool newton_mode, bool want_trace, ps_batch_status* status) {
+                     bool newton_mode, bool want_trace, ps_batch_status* status, bool probe_refill = false) {
   const DevProblem& P = ctx->P;
   if (count < 1 || count > ctx->max_batch) throw Failure(PS_ERR_BAD_ARG, "propagator: batch count out of range");
   if (!(dt > 0.0)) throw Failure(PS_ERR_BAD_ARG, "propagator: step size must be positive");
@@ -537,6 +537,7 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   K.chunk_rot = chunk_rotation();
   K.g_base = 0;
   K.hub_split = (geo.n_long == 1 && std::getenv("PPPC_NO_HUB_SPLIT") == nullptr) ? 1 : 0;
+  K.probe_refill = probe_refill ? 1 : 0;
   {
     // phase-A L2 prefetch distance in rows, PPPC_PF (default 0 = off: it helps
     // the standalone phase probe but not the persistent kernel)
@@ -1022,6 +1023,54 @@ int ps_newton_step(ps_ctx* ctx, int32_t count, const double* U_prev, const doubl
   });
 }
 
+// Test probe of the fused refill as the hot path runs
+// it: every system refills once at (u, u_prev, t_next, dt) inside the persistent
+// propagation kernel (refill_row_ell / refill_row / refill_long_rows /
+// refill_finish) and the kernel stops.  Outputs in the reference's order:
+// A = M/dt + J(u) [count][nnz] (per-system values where the kernel wrote them,
+// the shared step matrix on constant-nu rows), R = M (u - u_prev)/dt + K(u) u - f
+// [count][dim], Dinv = 1/diag(A) [count][dim].
+int ps_refill_probe(ps_ctx* ctx, int32_t count, const double* U, const double* U_prev, const double* t_next,
+                    double dt, double* A_out, double* R_out, double* Dinv_out) {
+  if (!ctx || !U || !U_prev || !t_next) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    const DevProblem& P = ctx->P;
+    if (count < 1 || count > ctx->max_batch) throw Failure(PS_ERR_BAD_ARG, "propagator: batch count out of range");
+    if (P.linear) throw Failure(PS_ERR_BAD_ARG, "probe: the refill probe needs an element (nonlinear) problem");
+    const int d = P.d, L = lanes_per_group(count);
+    stage_in_host(ctx, U_prev, count);
+    check(cudaMemcpyAsync(ctx->uprev, ctx->u, static_cast<size_t>(d) * lanes_padded(ctx) * sizeof(double),
+                          cudaMemcpyDeviceToDevice, ctx->stream),
+          "u_prev");
+    stage_in_host(ctx, U, count);
+    std::vector<double> t(t_next, t_next + count);
+    ps_batch_status st{};
+    propagate(ctx, count, 1, dt, t, true, false, &st, true);
+    const int G = (count + L - 1) / L;
+    std::vector<double> A(static_cast<size_t>(G) * P.nnz * 32), r(static_cast<size_t>(G) * d * 32),
+        di(static_cast<size_t>(G) * d * 32);
+    check(cudaMemcpy(A.data(), ctx->A, A.size() * sizeof(double), cudaMemcpyDeviceToHost), "A");
+    check(cudaMemcpy(r.data(), ctx->r, r.size() * sizeof(double), cudaMemcpyDeviceToHost), "r");
+    check(cudaMemcpy(di.data(), ctx->Dinv, di.size() * sizeof(double), cudaMemcpyDeviceToHost), "Dinv");
+    for (int n = 0; n < count; ++n) {
+      const int g = n / L, l = n % L;
+      for (int i = 0; i < d; ++i) {
+        const bool per_system = P.h_rowkind[i] != 0;
+        const size_t iv = (static_cast<size_t>(g) * d + i) * 32 + l;
+        double diag = 0.0;
+        for (int k = P.h_rp[i]; k < P.h_rp[i + 1]; ++k) {
+          const double a = per_system ? A[(static_cast<size_t>(g) * P.nnz + k) * 32 + l] : P.h_M[k] / dt + P.h_Kc[k];
+          if (A_out) A_out[static_cast<size_t>(n) * P.nnz + k] = a;
+          if (k == P.h_diag[i]) diag = a;
+        }
+        if (R_out) R_out[static_cast<size_t>(n) * d + i] = -r[iv];
+        if (Dinv_out) Dinv_out[static_cast<size_t>(n) * d + i] = per_system ? di[iv] : 1.0 / diag;
+      }
+    }
+  });
+}
+
 static int propagate_api(ps_ctx* ctx, int32_t n_first, int32_t count, const double* U_start, double* U_end,
                          ps_batch_status* status, bool fine, bool dev) {
   if (!ctx) return PS_ERR_BAD_ARG;
@@ -1193,6 +1242,37 @@ int ps_mh_setup(ps_ctx* ctx, int32_t use_conjugate_symmetry, const int32_t* bin_
   if (!ctx) return PS_ERR_BAD_ARG;
   std::lock_guard<std::mutex> lock(ctx->mu);
   return guard(ctx, [&] { ensure_spectral(ctx, use_conjugate_symmetry, bin_mask, shift_kind); });
+}
+
+// Test probes of the hot-path DFT kernels on the context's solved bins (after
+// ps_mh_setup): dft_forward_kernel and idft_jump_kernel + jump_finalize_kernel.
+int ps_mh_bins(ps_ctx* ctx, int32_t* bins, int32_t cap) {
+  if (!ctx) return -PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  if (!ctx->spec) return -PS_ERR_NOT_SETUP;
+  return spectral_bins(ctx->spec, bins, cap);
+}
+
+int ps_mh_forward(ps_ctx* ctx, const double* rhs, double* spectrum) {
+  if (!ctx || !rhs || !spectrum) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    if (!ctx->spec) throw Failure(PS_ERR_NOT_SETUP, "spectral: call ps_mh_setup first");
+    std::string err;
+    const int rc = spectral_forward_probe(ctx->spec, rhs, spectrum, &err);
+    if (rc != PS_OK) throw Failure(rc, err);
+  });
+}
+
+int ps_mh_inverse(ps_ctx* ctx, const double* spectrum, const double* U_old, double* U, double* jump) {
+  if (!ctx || !spectrum || !U) return PS_ERR_BAD_ARG;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return guard(ctx, [&] {
+    if (!ctx->spec) throw Failure(PS_ERR_NOT_SETUP, "spectral: call ps_mh_setup first");
+    std::string err;
+    const int rc = spectral_inverse_probe(ctx->spec, spectrum, U_old, U, jump, &err);
+    if (rc != PS_OK) throw Failure(rc, err);
+  });
 }
 
 int ps_assemble_rhs(ps_ctx* ctx, const double* F, const double* G, double* rhs) {

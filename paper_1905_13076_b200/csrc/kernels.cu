@@ -799,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     s.bt = s.zero_dx = false;
     s.newton_total = s.pcg_total = 0;
     s.max_nit = s.max_pit = s.last_nit = 0;
-    lact[lane] = valid ? (LINEAR ? ACT_L0 : ACT_R0) : ACT_IDLE;
+    lact[lane] = valid ? (LINEAR ? ACT_L0 : (P.probe_refill ? ACT_R : ACT_R0)) : ACT_IDLE;
     lstep[lane] = 0;
     if (lane == 0) any_a = 0, any_r = !LINEAR;
   }
@@ -974,7 +974,8 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
         t2v += qh * (dh * qh);
         if (c == __ldg(P.long_owner)) P.q[ih] = qh;
       }
-      switch (a) {
+      if (P.probe_refill) a = ACT_IDLE;  // the refill probe stops after its one refill
+      switch (P.probe_refill ? ACT_IDLE : a) {
         case ACT_R0: {
           s.tol = P.newton_tol_abs + P.newton_tol_rel * sqrt(t1v);
           s.nit = 1;

@@ -65,6 +65,7 @@ struct PropParams {
   int r_smem;            // 1: the PCG residual r of the block's rows (<= kLongRow slots) lives in shared memory
   int pf_dist;           // phase-A L2 prefetch distance in rows; 0 = off
   int hub_split;         // 1: the single long row's phase-A product goes through the reduction
+  int probe_refill;      // 1: every lane runs one refill (ACT_R, u vs uprev) and stops (ps_refill_probe)
   const double* M;
   const double* Klin;     // linear K (Newton on a linear problem)
   // shared step matrix M/dt + K (linear problems) or M/dt + K_const (element
@@ -193,6 +194,10 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
                    const double* rhs_il, double* U_il, double* U_prev_il, double* jump,
                    ps_batch_status* status, cudaStream_t st, std::string* err);
 int dft_forward_standalone(int n, int d, const double* U, double* spec, std::string* err);
+int spectral_forward_probe(SpectralState* s, const double* rhs, double* spec, std::string* err);
+int spectral_inverse_probe(SpectralState* s, const double* spec, const double* U_old, double* U, double* jump,
+                           std::string* err);
+int spectral_bins(const SpectralState* s, int32_t* bins, int32_t cap);
 int dft_inverse_standalone(int n, int d, const double* spec, double* U, std::string* err);
 int jump_norm_device(int count, int d, const double* cur_il, const double* prev_il, int stride,
                      double* out, cudaStream_t st);

@@ -1022,6 +1022,93 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
   return rc;
 }
 
+// Test probes of the hot-path spectral kernels with a context's solved bins
+// (ps_mh_forward / ps_mh_inverse): host arrays in the reference's order.
+// Forward: rhs [N][d] -> dft_forward_kernel -> spectrum [H][d] (complex pairs).
+int spectral_forward_probe(SpectralState* s, const double* rhs, double* spec, std::string* err) {
+  const int N = s->N, d = s->d, H = s->H;
+  if (H < 1) {
+    *err = "spectral: no solved bins";
+    return PS_ERR_BAD_ARG;
+  }
+  double* tmp = nullptr;
+  if (dalloc(&tmp, static_cast<size_t>(N) * d)) {
+    *err = "cuda: out of memory";
+    return PS_ERR_CUDA;
+  }
+  cudaMemcpy(tmp, rhs, static_cast<size_t>(N) * d * sizeof(double), cudaMemcpyHostToDevice);
+  launch_to_interleaved(tmp, s->rhs, N, d, N, nullptr);
+  const int ftpb = std::min(1024, ((kDftRows * H + 31) / 32) * 32);
+  dft_forward_kernel<<<s->idft_blocks, ftpb, dft_forward_smem(N, H)>>>(d, N, H, s->d_bins, s->tw, s->rhs, s->bhat);
+  cudaError_t e = cudaGetLastError();
+  std::vector<double2> h(static_cast<size_t>(d) * H);
+  if (e == cudaSuccess) e = cudaMemcpy(h.data(), s->bhat, h.size() * sizeof(double2), cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  if (e != cudaSuccess) {
+    *err = std::string("cuda: dft_forward failed: ") + cudaGetErrorString(e);
+    return PS_ERR_CUDA;
+  }
+  for (int hh = 0; hh < H; ++hh)
+    for (int i = 0; i < d; ++i) {
+      spec[(static_cast<size_t>(hh) * d + i) * 2] = h[static_cast<size_t>(i) * H + hh].x;
+      spec[(static_cast<size_t>(hh) * d + i) * 2 + 1] = h[static_cast<size_t>(i) * H + hh].y;
+    }
+  return PS_OK;
+}
+
+// Inverse: spectrum [H][d] -> idft_jump_kernel (mirror, realify check, jump
+// partials against U_old [N][d] or none) + jump_finalize_kernel -> U [N][d], jump.
+int spectral_inverse_probe(SpectralState* s, const double* spec, const double* U_old, double* U, double* jump,
+                           std::string* err) {
+  const int N = s->N, d = s->d, H = s->H;
+  std::vector<double2> h(static_cast<size_t>(d) * std::max(1, H));
+  for (int hh = 0; hh < H; ++hh)
+    for (int i = 0; i < d; ++i)
+      h[static_cast<size_t>(i) * H + hh] =
+          make_double2(spec[(static_cast<size_t>(hh) * d + i) * 2], spec[(static_cast<size_t>(hh) * d + i) * 2 + 1]);
+  double *tmp = nullptr, *u_il = nullptr, *old_il = nullptr;
+  if (dalloc(&tmp, static_cast<size_t>(N) * d) || dalloc(&u_il, static_cast<size_t>(N) * d) ||
+      dalloc(&old_il, static_cast<size_t>(N) * d)) {
+    *err = "cuda: out of memory";
+    return PS_ERR_CUDA;
+  }
+  if (H > 0) cudaMemcpy(s->x, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  if (U_old) {
+    cudaMemcpy(tmp, U_old, static_cast<size_t>(N) * d * sizeof(double), cudaMemcpyHostToDevice);
+    launch_to_interleaved(tmp, old_il, N, d, N, nullptr);
+  }
+  idft_jump_kernel<<<s->idft_blocks, idft_threads(N), idft_smem(N, H)>>>(
+      d, N, H, s->d_bins, s->tw, s->conj, s->x, u_il, U_old ? old_il : nullptr, s->jpart, s->maxre, s->maxim);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    jump_finalize_kernel<<<1, 1024>>>(N, s->idft_blocks, s->idft_blocks, s->jpart, s->maxre, s->maxim, s->jout);
+    e = cudaGetLastError();
+  }
+  double hj[5] = {0, 0, 0, 0, 0};
+  if (e == cudaSuccess) {
+    launch_from_interleaved(u_il, tmp, N, d, N, nullptr);
+    e = cudaMemcpy(U, tmp, static_cast<size_t>(N) * d * sizeof(double), cudaMemcpyDeviceToHost);
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(hj, s->jout, sizeof(hj), cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  cudaFree(u_il);
+  cudaFree(old_il);
+  if (e != cudaSuccess) {
+    *err = std::string("cuda: idft_jump failed: ") + cudaGetErrorString(e);
+    return PS_ERR_CUDA;
+  }
+  if (jump) *jump = hj[0];
+  if (!std::isfinite(hj[3]) || !std::isfinite(hj[4])) {
+    *err = "spectral: harmonic solve produced non-finite values";
+    return PS_ERR_NONFINITE;
+  }
+  if (hj[4] > kImagResidualTol * std::max(1.0, hj[3])) {
+    *err = "spectral: conjugate symmetry violated (imaginary residue " + std::to_string(hj[4]) + ")";
+    return PS_ERR_CONJ_SYMMETRY;
+  }
+  return PS_OK;
+}
+
 int dft_forward_standalone(int n, int d, const double* U, double* spec, std::string* err) {
   if (n < 2 || n % 2 != 0) {
     *err = "spectral: forward_dft requires an even number of blocks >= 2, got " + std::to_string(n);
@@ -1085,6 +1172,11 @@ int dft_inverse_standalone(int n, int d, const double* spec, double* U, std::str
   }
   for (size_t k = 0; k < total; ++k) U[k] = hout[k].x;
   return PS_OK;
+}
+
+int spectral_bins(const SpectralState* s, int32_t* bins, int32_t cap) {
+  for (int k = 0; k < s->H && k < cap; ++k) bins[k] = s->bins[k];
+  return s->H;
 }
 
 int jump_norm_device(int count, int d, const double* cur_il, const double* prev_il, int stride, double* out,

@@ -128,7 +128,8 @@ def test_excitation_frequency_validation_matches_reference():
 
 @pytest.mark.parametrize("kw", [dict(nr=2, ntheta=4), dict(nr=10, ntheta=16), dict(),
                                 dict(nr=12, ntheta=16, ripple_terms=5), dict(nr=40, ntheta=64, linear_sheath=1),
-                                dict(nr=200, ntheta=256), dict(nr=33, ntheta=7, return_in_sheath=0, current=20.0)])
+                                dict(nr=200, ntheta=256), dict(nr=33, ntheta=7, return_in_sheath=0, current=20.0),
+                                dict(nr=10, ntheta=40, r_conductor=1e-5, r_insulator=2e-5)])
 def test_oracle_builder_is_bit_identical(kw):
     """The oracle's own polar builder (oracle/polar_mesh.cpp) and the product
     builder (csrc/builders.cpp) are written independently; every array of the
