@@ -5,16 +5,16 @@
  * with no FFI; its hot path sits behind these C++ entry points, each of which is
  * replaced by one or more functions below (reference file:line in brackets):
  *
- *   PeriodicProblem(M, K_fn, J_fn, excitation)      [proj/include/parasteady/problem.hpp:133-162]
+ *   PeriodicProblem(M, K_fn, J_fn, excitation)      [proj/include/parasteady/problem.hpp:74-104]
  *        -> ps_problem_desc + ps_create
- *   newton_step(problem, u_prev, t_next, dt, s)     [proj/include/parasteady/propagators.hpp:256-257,
+ *   newton_step(problem, u_prev, t_next, dt, s)     [proj/include/parasteady/propagators.hpp:39-40,
  *                                                    proj/src/propagators.cpp:27-58]
  *        -> ps_newton_step
- *   Propagator::fine_propagate(n, u)                [proj/include/parasteady/propagators.hpp:276,
+ *   Propagator::fine_propagate(n, u)                [proj/include/parasteady/propagators.hpp:59,
  *                                                    proj/src/propagators.cpp:102-115]
  *        -> ps_fine_propagate_batch (all subintervals in one call; replaces the
  *           parallel_for at proj/src/engine.cpp:226-227)
- *   Propagator::coarse_propagate(n, u)              [proj/include/parasteady/propagators.hpp:275,
+ *   Propagator::coarse_propagate(n, u)              [proj/include/parasteady/propagators.hpp:58,
  *                                                    proj/src/propagators.cpp:96-100]
  *        -> ps_coarse_propagate_batch (replaces proj/src/engine.cpp:231-232 and :216)
  *   frozen_coarse_linearization(problem, ref)       [proj/src/engine.cpp:66-74]
@@ -78,7 +78,7 @@ enum {
 };
 
 /* ---------------------------------------------------------- problem data */
-/* Reluctivity curve [proj/include/parasteady/problem.hpp:97-118, proj/src/problem.cpp:65-98]:
+/* Reluctivity curve [proj/include/parasteady/problem.hpp:43-60, proj/src/problem.cpp:65-98]:
  * kind 0: constant nu; kind 1: Brauer nu(B^2) = min(k1*exp(min(k2*B^2,700)) + k3, 1/mu0). */
 typedef struct {
   int32_t kind;
@@ -88,7 +88,7 @@ typedef struct {
 } ps_curve;
 
 /* Structured description of  M u' + K(u) u = f(t),  u(0) = u(T)
- * [proj/include/parasteady/problem.hpp:123-162].  The opaque std::function
+ * [proj/include/parasteady/problem.hpp:74-104].  The opaque std::function
  * assembly callbacks of the reference cannot be offloaded, so the operator is
  * given by its elements instead:
  *     K(u) = sum_e nu(b2_e) S_e,   b2_e = u_e^T S_e u_e * inv_area_e,
@@ -340,7 +340,7 @@ int ps_polar_cable_defaults(ps_polar_cable_params* p);
 int ps_build_polar_cable(const ps_polar_cable_params* params, ps_problem** out);
 
 /* The reference's own 1-D radial coax cable, CoaxCableParams
- * [proj/include/parasteady/problem.hpp:181-203, proj/src/problem.cpp:242-361]. */
+ * [proj/include/parasteady/problem.hpp:122-144, proj/src/problem.cpp:242-361]. */
 typedef struct {
   int32_t n_r;
   int32_t source_region;

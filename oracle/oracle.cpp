@@ -22,7 +22,7 @@ namespace orc {
 
 using cd = std::complex<double>;
 constexpr double kPi = 3.14159265358979323846;
-// proj/include/parasteady/problem.hpp:121
+// proj/include/parasteady/problem.hpp:62
 constexpr double kVacuumReluctivity = 1.0 / (4.0e-7 * 3.14159265358979323846);
 // proj/src/spectral.cpp:21
 constexpr double kImagResidualTol = 1e-8;

@@ -139,7 +139,7 @@ class PeriodicProblem:
 
     Built either by the C++ builders (polar P1 cable, the reference's radial
     cable) or from explicit matrices for linear problems
-    (proj/include/parasteady/problem.hpp:123-162)."""
+    (proj/include/parasteady/problem.hpp:74-104)."""
 
     def __init__(self):
         self._handle = None

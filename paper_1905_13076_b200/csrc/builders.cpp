@@ -3,7 +3,7 @@
 // These produce the structured ps_problem_desc the device path consumes:
 //  * ps_build_radial_cable restates the reference's own 1-D radial coax cable
 //    (proj/src/problem.cpp:242-361, CoaxCableParams at
-//    proj/include/parasteady/problem.hpp:181-203) as 2-node elements, so the
+//    proj/include/parasteady/problem.hpp:122-144) as 2-node elements, so the
 //    reference's cable tests run through the GPU path;
 //  * ps_build_polar_cable builds the 2-D structured polar P1 cable that
 //    BASELINE.json's configs name (canonical mesh: SURVEY.md App. A.1).
@@ -21,7 +21,7 @@
 namespace {
 
 constexpr double kPi = 3.14159265358979323846;
-// proj/include/parasteady/problem.hpp:121
+// proj/include/parasteady/problem.hpp:62
 constexpr double kVacuumReluctivity = 1.0 / (4.0e-7 * 3.14159265358979323846);
 
 thread_local std::string g_builder_error;
@@ -142,7 +142,7 @@ extern "C" {
 int ps_radial_cable_defaults(ps_radial_cable_params* p) {
   if (!p) return PS_ERR_BAD_ARG;
   std::memset(p, 0, sizeof(*p));
-  // proj/include/parasteady/problem.hpp:181-196
+  // proj/include/parasteady/problem.hpp:122-137
   p->n_r = 200;
   p->r1 = 2.0e-3;
   p->r2 = 3.5e-3;
@@ -508,7 +508,10 @@ void ps_seeded_uniform(uint64_t seed, int64_t count, double lo, double hi, doubl
 // (SURVEY.md §8f ranks 2-3).  Host C++, no third-party parser: a restatement of
 // proj/src/matrix_market.cpp:30-98, proj/src/problem.cpp:363-421 (the JSON
 // schema nlohmann::json parses there) and proj/src/io.cpp:151-178.
+#include <cerrno>
 #include <charconv>
+#include <cstdlib>
+#include <string_view>
 #include <fstream>
 #include <map>
 #include <memory>
@@ -558,49 +561,99 @@ ps_csr to_csr(int32_t rows, int32_t cols, std::vector<Trip> t) {
   return m;
 }
 
-// read_matrix_market (proj/src/matrix_market.cpp:30-81)
+// Matrix Market coordinate files (the subset read_matrix_market accepts,
+// proj/src/matrix_market.cpp:30-81: real, general or symmetric, 1-based).  The
+// file is read whole and walked by a cursor over its data lines; numbers are
+// parsed with strtol / strtod so a stray token anywhere in a line is an error.
+class MMCursor {
+ public:
+  MMCursor(std::string text, std::string path) : text_(std::move(text)), path_(std::move(path)) {}
+
+  [[noreturn]] void fail(const std::string& what) const { throw std::runtime_error("matrix_market: " + what + path_); }
+
+  // next line (without the newline); false at end of file
+  bool line(std::string_view* out) {
+    if (pos_ >= text_.size()) return false;
+    const size_t nl = text_.find('\n', pos_);
+    const size_t end = nl == std::string::npos ? text_.size() : nl;
+    *out = std::string_view(text_).substr(pos_, end - pos_);
+    if (!out->empty() && out->back() == '\r') out->remove_suffix(1);
+    pos_ = end + 1;
+    return true;
+  }
+  // next line that is neither blank nor a % comment
+  bool data_line(std::string_view* out) {
+    while (line(out)) {
+      const size_t k = out->find_first_not_of(" \t");
+      if (k != std::string_view::npos && (*out)[k] != '%') return true;
+    }
+    return false;
+  }
+
+ private:
+  std::string text_, path_;
+  size_t pos_ = 0;
+};
+
+// whitespace-separated fields of one line; exactly `n` of them must parse
+bool mm_fields(std::string_view ln, int n, long* ints, double* real) {
+  std::string buf(ln);
+  const char* c = buf.c_str();
+  for (int f = 0; f < n; ++f) {
+    char* end = nullptr;
+    errno = 0;
+    if (real && f == n - 1) {
+      *real = std::strtod(c, &end);
+    } else {
+      ints[f] = std::strtol(c, &end, 10);
+    }
+    if (end == c || errno != 0 || (*end != '\0' && *end != ' ' && *end != '\t')) return false;
+    c = end;
+  }
+  while (*c == ' ' || *c == '\t') ++c;
+  return *c == '\0';
+}
+
 ps_csr read_mm(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) throw std::runtime_error("matrix_market: cannot open " + path);
-  std::string header;
-  if (!std::getline(in, header)) throw std::runtime_error("matrix_market: empty file " + path);
-  std::istringstream hs(header);
-  std::string banner, object, format, field, symmetry;
-  hs >> banner >> object >> format >> field >> symmetry;
-  if (banner != "%%MatrixMarket" || lower(object) != "matrix")
-    throw std::runtime_error("matrix_market: bad header in " + path);
-  if (lower(format) != "coordinate") throw std::runtime_error("matrix_market: only coordinate format is supported");
-  if (lower(field) != "real") throw std::runtime_error("matrix_market: only real matrices are supported");
-  const std::string sym = lower(symmetry);
-  if (sym != "general" && sym != "symmetric")
-    throw std::runtime_error("matrix_market: only general or symmetric storage is supported");
-  std::string line;
-  long rows = -1, cols = -1, nnz = -1;
-  while (std::getline(in, line)) {
-    if (line.empty() || line[0] == '%') continue;
-    std::istringstream ls(line);
-    if (!(ls >> rows >> cols >> nnz)) throw std::runtime_error("matrix_market: malformed size line in " + path);
-    break;
+  std::ifstream file(path, std::ios::binary);
+  if (!file) throw std::runtime_error("matrix_market: cannot open " + path);
+  std::ostringstream whole;
+  whole << file.rdbuf();
+  MMCursor cur(whole.str(), " in " + path);
+  std::string_view first;
+  if (!cur.line(&first)) cur.fail("empty file");
+  // banner: %%MatrixMarket matrix <format> <field> <symmetry>
+  std::vector<std::string> word;
+  {
+    std::istringstream ws{std::string(first)};
+    for (std::string w; ws >> w;) word.push_back(lower(w));
   }
-  if (rows < 0 || cols < 0 || nnz < 0) throw std::runtime_error("matrix_market: missing size line in " + path);
-  std::vector<Trip> trips;
-  trips.reserve(static_cast<size_t>(sym == "symmetric" ? 2 * nnz : nnz));
-  long seen = 0;
-  while (seen < nnz && std::getline(in, line)) {
-    if (line.empty() || line[0] == '%') continue;
-    std::istringstream ls(line);
-    long i, j;
-    double v;
-    if (!(ls >> i >> j >> v)) throw std::runtime_error("matrix_market: malformed entry in " + path);
-    if (i < 1 || i > rows || j < 1 || j > cols) throw std::runtime_error("matrix_market: index out of range in " + path);
-    trips.push_back({static_cast<int32_t>(i - 1), static_cast<int32_t>(j - 1), v});
-    if (sym == "symmetric" && i != j) trips.push_back({static_cast<int32_t>(j - 1), static_cast<int32_t>(i - 1), v});
-    ++seen;
+  if (word.size() < 5 || word[0] != "%%matrixmarket" || word[1] != "matrix") cur.fail("bad header");
+  if (word[2] != "coordinate") cur.fail("only coordinate format is supported");
+  if (word[3] != "real") cur.fail("only real matrices are supported");
+  const bool mirrored = word[4] == "symmetric";
+  if (!mirrored && word[4] != "general") cur.fail("only general or symmetric storage is supported");
+  std::string_view ln;
+  long shape[3];
+  if (!cur.data_line(&ln)) cur.fail("missing size line");
+  if (!mm_fields(ln, 3, shape, nullptr) || shape[0] < 0 || shape[1] < 0 || shape[2] < 0)
+    cur.fail("malformed size line");
+  const long n_rows = shape[0], n_cols = shape[1], declared = shape[2];
+  std::vector<Trip> entries;
+  entries.reserve(static_cast<size_t>(mirrored ? 2 * declared : declared));
+  long read = 0;
+  for (; read < declared && cur.data_line(&ln); ++read) {
+    long ij[2];
+    double v = 0.0;
+    if (!mm_fields(ln, 3, ij, &v)) cur.fail("malformed entry");
+    if (ij[0] < 1 || ij[0] > n_rows || ij[1] < 1 || ij[1] > n_cols) cur.fail("index out of range");
+    const auto r = static_cast<int32_t>(ij[0] - 1), c = static_cast<int32_t>(ij[1] - 1);
+    entries.push_back({r, c, v});
+    if (mirrored && r != c) entries.push_back({c, r, v});
   }
-  if (seen != nnz)
-    throw std::runtime_error("matrix_market: expected " + std::to_string(nnz) + " entries, got " +
-                             std::to_string(seen) + " in " + path);
-  return to_csr(static_cast<int32_t>(rows), static_cast<int32_t>(cols), std::move(trips));
+  if (read != declared)
+    cur.fail("expected " + std::to_string(declared) + " entries, got " + std::to_string(read));
+  return to_csr(static_cast<int32_t>(n_rows), static_cast<int32_t>(n_cols), std::move(entries));
 }
 
 // ---- a small JSON reader for the excitation schema
