@@ -145,9 +145,11 @@ typedef struct {
 } ps_newton_settings;
 
 typedef struct {
-  double tol_rel;   /* stop at ||r||_2 <= tol_rel * ||b||_2 (1e-12) */
-  int32_t max_iter; /* 20000 */
-  int32_t pad_;
+  double tol_rel;     /* stop at ||r||_2 <= tol_rel * ||b||_2 (1e-12) */
+  int32_t max_iter;   /* 20000 */
+  int32_t warm_start; /* COCG only: start each multiharmonic solve of a context from the
+                         solution of its previous successful solve (0 = from zero; the
+                         reference's direct solve has no start value) */
 } ps_krylov_settings;
 
 typedef struct {
@@ -266,6 +268,9 @@ typedef struct {
   int64_t fine_pcg_iterations, coarse_pcg_iterations, cocg_iterations, newton_iterations;
   double fine_bytes;               /* canonical algorithmic bytes of the fine kernels */
   double final_defect;             /* PP-IC: relative_defect(u_N, u_0) of the last iterate */
+  int64_t cocg_per_iteration[PS_MAX_HISTORY];  /* PP-PC: COCG iterations (all bins) per iteration */
+  double fine_ms_per_iteration[PS_MAX_HISTORY];
+  double spectral_ms_per_iteration[PS_MAX_HISTORY];
 } ps_history;
 
 /* solve_pp_pc with the multiharmonic coarse solver [proj/src/engine.cpp:187-270].

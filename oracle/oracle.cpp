@@ -391,17 +391,29 @@ struct KrylovFailure {
 
 template <class S, class MatVec>
 int jacobi_cg(const Problem& p, MatVec matvec, const S* dinv, const S* b, S* x, double tol,
-              int max_iter) {
+              int max_iter, bool warm = false) {
+  // warm: x holds the start value (r = b - A x; the stop stays relative to b, and
+  // a start that already meets it takes no iteration); cold: x = 0, r = b
   const int n = p.d;
   std::vector<S> r(b, b + n), z(n), pv(n), q(n);
-  std::fill(x, x + n, S(0));
+  double bb = 0.0;
+  for (int i = 0; i < n; ++i) bb += abs2(b[i]);
+  if (warm && bb != 0.0) {
+    matvec(x, q.data());
+    for (int i = 0; i < n; ++i) r[i] = b[i] - q[i];
+  } else {
+    std::fill(x, x + n, S(0));
+  }
   for (int i = 0; i < n; ++i) z[i] = dinv[i] * r[i];
   pv = z;
   S rho = dotu(r.data(), z.data(), n);
-  double bb = 0.0;
-  for (int i = 0; i < n; ++i) bb += abs2(r[i]);
   if (bb == 0.0) return 0;
   const double stop = (tol * tol) * bb;
+  if (warm) {
+    double rr0 = 0.0;
+    for (int i = 0; i < n; ++i) rr0 += abs2(r[i]);
+    if (rr0 <= stop) return 0;
+  }
   int it = 0;
   for (;;) {
     matvec(pv.data(), q.data());
@@ -714,9 +726,12 @@ void assemble_rhs(const Problem& lin, const Mesh& mesh, const double* F, const d
 
 // MultiharmonicCyclicSolver (proj/src/spectral.cpp:224-279) with the bin mask
 // and shift-kind extensions of SURVEY.md App. A.3/A.4.
+// warm (ITERATIVE, s.cocg.warm_start): the previous solve's spectrum, used as
+// the COCG start value of every solved bin and replaced by this solve's
+// (empty on the first solve: cold start).
 void mh_solve(const Problem& lin, const Mesh& mesh, const ps_solver_settings& s, int mode,
               bool conj, const int32_t* mask, int shift_kind, const double* rhs, double* U,
-              int workers, int64_t* cocg_iters) {
+              int workers, int64_t* cocg_iters, std::vector<cd>* warm = nullptr) {
   const int n = mesh.N, d = lin.d;
   require_even_blocks(n, "multiharmonic solve");
   const double dT = mesh.coarse_dt();
@@ -726,6 +741,8 @@ void mh_solve(const Problem& lin, const Mesh& mesh, const ps_solver_settings& s,
     Q[k] = C[k] + lin.K[k];
   }
   std::vector<cd> in(static_cast<int64_t>(n) * d), hat(in.size()), sol(in.size(), cd(0, 0)), back(in.size());
+  const bool warm_start = warm && s.cocg.warm_start && mode != OR_DIRECT && warm->size() == sol.size();
+  if (warm_start) sol = *warm;
   for (int64_t i = 0; i < static_cast<int64_t>(in.size()); ++i) in[i] = cd(rhs[i], 0.0);
   dft_bins(n, d, in.data(), hat.data(), -1);
   const int last = conj ? n / 2 : n - 1;
@@ -763,7 +780,7 @@ void mh_solve(const Problem& lin, const Mesh& mesh, const ps_solver_settings& s,
         }
       };
       try {
-        its[bin] = jacobi_cg<cd>(lin, mv, dinv.data(), b, x, s.cocg.tol_rel, s.cocg.max_iter);
+        its[bin] = jacobi_cg<cd>(lin, mv, dinv.data(), b, x, s.cocg.tol_rel, s.cocg.max_iter, warm_start);
       } catch (const KrylovFailure& kf) {
         std::ostringstream msg;
         if (kf.kind == 0) {
@@ -779,6 +796,7 @@ void mh_solve(const Problem& lin, const Mesh& mesh, const ps_solver_settings& s,
         throw Error(PS_ERR_NONFINITE, "spectral: harmonic solve produced non-finite values");
   });
   if (cocg_iters) *cocg_iters += std::accumulate(its.begin(), its.end(), int64_t{0});
+  if (warm && s.cocg.warm_start && mode != OR_DIRECT) *warm = sol;
   if (conj)
     for (int bin = n / 2 + 1; bin < n; ++bin)
       for (int i = 0; i < d; ++i)
@@ -1054,6 +1072,7 @@ int or_pppc_solve(const or_problem* p, const ps_time_mesh* mesh, const ps_solver
     for (int n = 1; n < n_sub; ++n)
       coarse.coarse_propagate(n, &u[static_cast<int64_t>(n - 1) * d], &u[static_cast<int64_t>(n) * d], &sweep);
     h.coarse_pcg_iterations += sweep.pcg;
+    std::vector<cd> warm;  // the previous iteration's spectrum (COCG warm start)
     for (int k = 0; k < e->max_iterations; ++k) {
       std::vector<StepOut> fo(n_sub), co(n_sub);
       parallel_for(n_sub, workers, [&](int i) {
@@ -1070,8 +1089,9 @@ int or_pppc_solve(const or_problem* p, const ps_time_mesh* mesh, const ps_solver
       assemble_rhs(*coarse_problem, m, fine_end.data(), coarse_end.data(), rhs.data());
       int64_t cocg = 0;
       mh_solve(*coarse_problem, m, *s, mode, e->use_conjugate_symmetry != 0, e->bin_mask, e->shift_kind,
-               rhs.data(), next.data(), workers, &cocg);
+               rhs.data(), next.data(), workers, &cocg, &warm);
       h.cocg_iterations += cocg;
+      if (k < PS_MAX_HISTORY) h.cocg_per_iteration[k] = cocg;
       const double jump = jump_norm(n_sub, d, next.data(), u.data());
       if (k < PS_MAX_HISTORY) h.jumps[k] = jump;
       h.iterations = k + 1;

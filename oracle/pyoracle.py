@@ -304,7 +304,9 @@ class Oracle:
         hist = dict(iterations=h.iterations, converged=bool(h.converged),
                     jumps=[h.jumps[k] for k in range(min(h.iterations, _abi.PS_MAX_HISTORY))],
                     fine_pcg_iterations=h.fine_pcg_iterations, coarse_pcg_iterations=h.coarse_pcg_iterations,
-                    cocg_iterations=h.cocg_iterations, newton_iterations=h.newton_iterations)
+                    cocg_iterations=h.cocg_iterations, newton_iterations=h.newton_iterations,
+                    cocg_per_iteration=[h.cocg_per_iteration[k]
+                                        for k in range(min(h.iterations, _abi.PS_MAX_HISTORY))])
         return U, hist, (its[:h.iterations] if its is not None else None)
 
     def _parareal(self, settings, u0, mode, keep_iterates, workers):

@@ -60,7 +60,7 @@ class ps_newton_settings(C.Structure):
 
 
 class ps_krylov_settings(C.Structure):
-    _fields_ = [("tol_rel", C.c_double), ("max_iter", C.c_int32), ("pad_", C.c_int32)]
+    _fields_ = [("tol_rel", C.c_double), ("max_iter", C.c_int32), ("warm_start", C.c_int32)]
 
 
 class ps_solver_settings(C.Structure):
@@ -92,7 +92,10 @@ class ps_history(C.Structure):
                 ("total_ms", C.c_double), ("fine_pcg_iterations", C.c_int64),
                 ("coarse_pcg_iterations", C.c_int64), ("cocg_iterations", C.c_int64),
                 ("newton_iterations", C.c_int64), ("fine_bytes", C.c_double),
-                ("final_defect", C.c_double)]
+                ("final_defect", C.c_double),
+                ("cocg_per_iteration", C.c_int64 * PS_MAX_HISTORY),
+                ("fine_ms_per_iteration", C.c_double * PS_MAX_HISTORY),
+                ("spectral_ms_per_iteration", C.c_double * PS_MAX_HISTORY)]
 
 
 class ps_polar_cable_params(C.Structure):

@@ -101,6 +101,8 @@ class NewtonSettings:
 class KrylovSettings:
     tol_rel: float = 1e-12
     max_iter: int = 20000
+    # COCG only: start a context's multiharmonic solve from its previous solution
+    warm_start: bool = False
 
 
 def solver_settings(newton: Optional[NewtonSettings] = None, pcg: Optional[KrylovSettings] = None,
@@ -114,6 +116,7 @@ def solver_settings(newton: Optional[NewtonSettings] = None, pcg: Optional[Krylo
     s.newton.line_search = newton.line_search
     s.pcg.tol_rel, s.pcg.max_iter = pcg.tol_rel, pcg.max_iter
     s.cocg.tol_rel, s.cocg.max_iter = cocg.tol_rel, cocg.max_iter
+    s.cocg.warm_start = 1 if cocg.warm_start else 0
     s.max_batch = max_batch
     return s
 
@@ -773,7 +776,12 @@ def solve_pp_pc(problem: PeriodicProblem, settings: EngineSettings, keep_iterate
                     fine_ms=h.fine_ms, coarse_ms=h.coarse_ms, spectral_ms=h.spectral_ms, total_ms=h.total_ms,
                     fine_pcg_iterations=h.fine_pcg_iterations, coarse_pcg_iterations=h.coarse_pcg_iterations,
                     cocg_iterations=h.cocg_iterations, newton_iterations=h.newton_iterations,
-                    fine_bytes=h.fine_bytes)
+                    fine_bytes=h.fine_bytes,
+                    cocg_per_iteration=[h.cocg_per_iteration[k] for k in range(min(h.iterations, _abi.PS_MAX_HISTORY))],
+                    fine_ms_per_iteration=[h.fine_ms_per_iteration[k]
+                                           for k in range(min(h.iterations, _abi.PS_MAX_HISTORY))],
+                    spectral_ms_per_iteration=[h.spectral_ms_per_iteration[k]
+                                               for k in range(min(h.iterations, _abi.PS_MAX_HISTORY))])
         return PeriodicSolveResult(U, hist, its[:h.iterations] if its is not None else None)
     finally:
         prop.close()

@@ -1465,7 +1465,12 @@ int ps_pppc_solve(ps_ctx* fine, const ps_engine_settings* settings, const double
       if (src != PS_OK) throw Failure(src, err);
       h.spectral_ms += ss.kernel_ms;
       h.cocg_iterations += ss.pcg_iterations;
-      if (k < PS_MAX_HISTORY) h.jumps[k] = jump;
+      if (k < PS_MAX_HISTORY) {
+        h.jumps[k] = jump;
+        h.cocg_per_iteration[k] = ss.pcg_iterations;
+        h.fine_ms_per_iteration[k] = fs.kernel_ms;
+        h.spectral_ms_per_iteration[k] = ss.kernel_ms;
+      }
       h.iterations = k + 1;
       if (iterates) {
         launch_from_interleaved(U, fine->io_b, N, d, N, coarse->stream);

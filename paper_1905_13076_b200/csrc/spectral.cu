@@ -60,6 +60,7 @@ struct CocgParams {
   double2* q;
   double tol;
   int max_iter;
+  int warm;        // 1: x holds the start value (the previous solve's solution)
   unsigned long long* sync;
   double* partials;
   int* abort_flag;
@@ -115,6 +116,112 @@ __device__ __forceinline__ void cocg_row_a(const CocgParams& P, int i, const int
   acc[5] += qdq.y;
 }
 
+// Phase A of one COCG iteration for this thread's rows: q = Lambda p and the
+// partials p.q, q.z, q.Dq.  Called by every thread of the block (the long-row
+// path uses block barriers); `act`: this lane's bin is iterating.
+__device__ __forceinline__ void cocg_phase_a(const CocgParams& P, bool act, int c, int row_begin, int row_end,
+                                             size_t H, int h, double2 s_b, double2 (*lpart)[32],
+                                             double (&acc)[kCND]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / P.Lp;
+  // long rows (the polar hub): slots split across the owning block's warps
+  for (int j = 0; j < P.n_long; ++j) {
+    if (__ldg(P.long_owner + j) != c) continue;
+    const int i = __ldg(P.long_rows + j);
+    const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+    double2 part = make_double2(0.0, 0.0);
+    if (act)
+      for (int k = base + warp; k < end; k += kWarps) {
+        const int cj = __ldg(P.ci + k);
+        const double xk = __ldg(P.X + k), yk = __ldg(P.Y + k);
+        part = cadd(part, cmul(make_double2(xk + s_b.x * yk, s_b.y * yk), P.p[static_cast<size_t>(cj) * H + h]));
+      }
+    lpart[warp][lane] = part;
+    __syncthreads();
+    if (warp == 0 && act) {
+      double2 qv = make_double2(0.0, 0.0);
+      for (int w = 0; w < kWarps; ++w) qv = cadd(qv, lpart[w][lane]);
+      const size_t iv = static_cast<size_t>(i) * H + h;
+      P.q[iv] = qv;
+      const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
+      const double2 pi = P.p[iv], ri = P.r[iv];
+      const double2 zi = cmul(dinv, ri);
+      const double2 pq = cmul(pi, qv), qz = cmul(qv, zi), qdq = cmul(qv, cmul(dinv, qv));
+      acc[0] += pq.x;
+      acc[1] += pq.y;
+      acc[2] += qz.x;
+      acc[3] += qz.y;
+      acc[4] += qdq.x;
+      acc[5] += qdq.y;
+    }
+    __syncthreads();
+  }
+  if (act && row_begin + sub < row_end) {
+    // row records two rows ahead of their use; the next row's gathered p
+    // entries, own p / r and slot values are requested into L1 one row ahead
+    // (no registers held), so the row's loads mostly hit L1
+    int i = row_begin + sub;
+    int4 h0 = __ldg(P.rowrec + kRecInts4 * i), c03 = __ldg(P.rowrec + kRecInts4 * i + 1),
+         c47 = __ldg(P.rowrec + kRecInts4 * i + 2);
+    int4 h1 = h0, d03 = c03, d47 = c47;
+    if (i + P.R < row_end) {
+      h1 = __ldg(P.rowrec + kRecInts4 * (i + P.R));
+      d03 = __ldg(P.rowrec + kRecInts4 * (i + P.R) + 1);
+      d47 = __ldg(P.rowrec + kRecInts4 * (i + P.R) + 2);
+    }
+    for (;;) {
+      const int i1 = i + P.R, i2 = i + 2 * P.R;
+      const bool more = i1 < row_end;
+      int4 h2 = h1, e03 = d03, e47 = d47;
+      if (i2 < row_end) {
+        h2 = __ldg(P.rowrec + kRecInts4 * i2);
+        e03 = __ldg(P.rowrec + kRecInts4 * i2 + 1);
+        e47 = __ldg(P.rowrec + kRecInts4 * i2 + 2);
+      }
+      if (more && h1.y <= kEll) {
+        const int cn[kEll] = {d03.x, d03.y, d03.z, d03.w, d47.x, d47.y, d47.z, d47.w};
+#pragma unroll
+        for (int k = 0; k < kEll; ++k)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(P.p + static_cast<size_t>(cn[k]) * H + h));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(P.r + static_cast<size_t>(i1) * H + h));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(P.XYE + static_cast<size_t>(i1) * kEll));
+      }
+      const int len = h0.y;
+      if (len <= kEll) {
+        cocg_row_a(P, i, c03, c47, H, h, s_b, acc);
+      } else if (len <= kLongRow) {
+        double2 qv = make_double2(0.0, 0.0);
+        for (int k = h0.x; k < h0.x + len; ++k) {
+          const int j = __ldg(P.ci + k);
+          const double xk = __ldg(P.X + k), yk = __ldg(P.Y + k);
+          const double2 lam = make_double2(xk + s_b.x * yk, s_b.y * yk);
+          qv = cadd(qv, cmul(lam, P.p[static_cast<size_t>(j) * H + h]));
+        }
+        const size_t iv = static_cast<size_t>(i) * H + h;
+        P.q[iv] = qv;
+        const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
+        const double2 pi = P.p[iv], ri = P.r[iv];
+        const double2 zi = cmul(dinv, ri);
+        const double2 pq = cmul(pi, qv), qz = cmul(qv, zi), qdq = cmul(qv, cmul(dinv, qv));
+        acc[0] += pq.x;
+        acc[1] += pq.y;
+        acc[2] += qz.x;
+        acc[3] += qz.y;
+        acc[4] += qdq.x;
+        acc[5] += qdq.y;
+      }
+      if (!more) break;
+      i = i1;
+      h0 = h1;
+      c03 = d03;
+      c47 = d47;
+      h1 = h2;
+      d03 = e03;
+      d47 = e47;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
   __shared__ SyncShared<kCND> sh;
   __shared__ double2 lpart[kWarps][32];
@@ -148,126 +255,48 @@ __global__ void __launch_bounds__(kThreads, 1) cocg_kernel(const CocgParams P) {
   s.stop = 0.0;
   long long lockstep = 0;
 
-  // init: x = 0, r = b, z = D r, p = z, rho = r.z, bb = |r|^2
+  if (P.warm) {
+    // warm start from x (the previous solve's solution): q = Lambda x with the
+    // phase-A rows reading x in place of p; each row's q is read back below by
+    // the thread of the same block that owns the row
+    CocgParams Pw = P;
+    Pw.p = P.x;
+    cocg_phase_a(Pw, s.alive, c, row_begin, row_end, H, h, s_b, lpart, acc);
+#pragma unroll
+    for (int k = 0; k < kCND; ++k) acc[k] = 0.0;
+    __syncthreads();
+  }
+  // init: r = b - Lambda x (x = 0 cold: r = b), z = D r, p = z, rho = r.z,
+  // bb = |b|^2 (the stop stays relative to b), rr = |r|^2
   if (s.alive)
     for (int i = row_begin + sub; i < row_end; i += P.R) {
       const size_t iv = static_cast<size_t>(i) * H + h;
       const double2 bv = P.b[iv];
+      const double2 rv = P.warm ? csub(bv, P.q[iv]) : bv;
       const double2 z = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
-      const double2 zr = cmul(z, bv);
-      P.x[iv] = make_double2(0.0, 0.0);
-      P.r[iv] = bv;
+      const double2 zr = cmul(z, rv);
+      if (!P.warm) P.x[iv] = make_double2(0.0, 0.0);
+      P.r[iv] = rv;
       P.p[iv] = zr;
-      const double2 rz = cmul(bv, zr);
+      const double2 rz = cmul(rv, zr);
       acc[0] += rz.x;
       acc[1] += rz.y;
       acc[2] += bv.x * bv.x + bv.y * bv.y;
+      acc[3] += rv.x * rv.x + rv.y * rv.y;
     }
-  if (!group_sync_reduce<kCND, 3>(X, sh, acc, g, c)) return;
+  if (!group_sync_reduce<kCND, 4>(X, sh, acc, g, c)) return;
   if (s.alive) {
     s.rho = make_double2(sh.tot[0][sl], sh.tot[1][sl]);
-    const double bb = sh.tot[2][sl];
+    const double bb = sh.tot[2][sl], rr = sh.tot[3][sl];
     s.stop = (P.tol * P.tol) * bb;
-    s.act = bb != 0.0;
+    // cold: at least one iteration unless b = 0; warm: none if x already meets the stop
+    s.act = P.warm ? (bb != 0.0 && !(rr <= s.stop)) : bb != 0.0;
+    if (P.warm && bb == 0.0)
+      for (int i = row_begin + sub; i < row_end; i += P.R) P.x[static_cast<size_t>(i) * H + h] = make_double2(0.0, 0.0);
   }
 
   while (__syncthreads_or(s.act ? 1 : 0)) {
-    // long rows (the polar hub): slots split across the owning block's warps
-    for (int j = 0; j < P.n_long; ++j) {
-      if (__ldg(P.long_owner + j) != c) continue;
-      const int i = __ldg(P.long_rows + j);
-      const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
-      double2 part = make_double2(0.0, 0.0);
-      if (s.act)
-        for (int k = base + warp; k < end; k += kWarps) {
-          const int cj = __ldg(P.ci + k);
-          const double xk = __ldg(P.X + k), yk = __ldg(P.Y + k);
-          part = cadd(part, cmul(make_double2(xk + s_b.x * yk, s_b.y * yk), P.p[static_cast<size_t>(cj) * H + h]));
-        }
-      lpart[warp][lane] = part;
-      __syncthreads();
-      if (warp == 0 && s.act) {
-        double2 qv = make_double2(0.0, 0.0);
-        for (int w = 0; w < kWarps; ++w) qv = cadd(qv, lpart[w][lane]);
-        const size_t iv = static_cast<size_t>(i) * H + h;
-        P.q[iv] = qv;
-        const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
-        const double2 pi = P.p[iv], ri = P.r[iv];
-        const double2 zi = cmul(dinv, ri);
-        const double2 pq = cmul(pi, qv), qz = cmul(qv, zi), qdq = cmul(qv, cmul(dinv, qv));
-        acc[0] += pq.x;
-        acc[1] += pq.y;
-        acc[2] += qz.x;
-        acc[3] += qz.y;
-        acc[4] += qdq.x;
-        acc[5] += qdq.y;
-      }
-      __syncthreads();
-    }
-    if (s.act && row_begin + sub < row_end) {
-      // row records two rows ahead of their use; the next row's gathered p
-      // entries, own p / r and slot values are requested into L1 one row ahead
-      // (no registers held), so the row's loads mostly hit L1
-      int i = row_begin + sub;
-      int4 h0 = __ldg(P.rowrec + kRecInts4 * i), c03 = __ldg(P.rowrec + kRecInts4 * i + 1),
-           c47 = __ldg(P.rowrec + kRecInts4 * i + 2);
-      int4 h1 = h0, d03 = c03, d47 = c47;
-      if (i + P.R < row_end) {
-        h1 = __ldg(P.rowrec + kRecInts4 * (i + P.R));
-        d03 = __ldg(P.rowrec + kRecInts4 * (i + P.R) + 1);
-        d47 = __ldg(P.rowrec + kRecInts4 * (i + P.R) + 2);
-      }
-      for (;;) {
-        const int i1 = i + P.R, i2 = i + 2 * P.R;
-        const bool more = i1 < row_end;
-        int4 h2 = h1, e03 = d03, e47 = d47;
-        if (i2 < row_end) {
-          h2 = __ldg(P.rowrec + kRecInts4 * i2);
-          e03 = __ldg(P.rowrec + kRecInts4 * i2 + 1);
-          e47 = __ldg(P.rowrec + kRecInts4 * i2 + 2);
-        }
-        if (more && h1.y <= kEll) {
-          const int cn[kEll] = {d03.x, d03.y, d03.z, d03.w, d47.x, d47.y, d47.z, d47.w};
-#pragma unroll
-          for (int k = 0; k < kEll; ++k)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(P.p + static_cast<size_t>(cn[k]) * H + h));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(P.r + static_cast<size_t>(i1) * H + h));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(P.XYE + static_cast<size_t>(i1) * kEll));
-        }
-        const int len = h0.y;
-        if (len <= kEll) {
-          cocg_row_a(P, i, c03, c47, H, h, s_b, acc);
-        } else if (len <= kLongRow) {
-          double2 qv = make_double2(0.0, 0.0);
-          for (int k = h0.x; k < h0.x + len; ++k) {
-            const int j = __ldg(P.ci + k);
-            const double xk = __ldg(P.X + k), yk = __ldg(P.Y + k);
-            const double2 lam = make_double2(xk + s_b.x * yk, s_b.y * yk);
-            qv = cadd(qv, cmul(lam, P.p[static_cast<size_t>(j) * H + h]));
-          }
-          const size_t iv = static_cast<size_t>(i) * H + h;
-          P.q[iv] = qv;
-          const double2 dinv = cdiv(make_double2(1.0, 0.0), lam_diag(P, i, s_b));
-          const double2 pi = P.p[iv], ri = P.r[iv];
-          const double2 zi = cmul(dinv, ri);
-          const double2 pq = cmul(pi, qv), qz = cmul(qv, zi), qdq = cmul(qv, cmul(dinv, qv));
-          acc[0] += pq.x;
-          acc[1] += pq.y;
-          acc[2] += qz.x;
-          acc[3] += qz.y;
-          acc[4] += qdq.x;
-          acc[5] += qdq.y;
-        }
-        if (!more) break;
-        i = i1;
-        h0 = h1;
-        c03 = d03;
-        c47 = d47;
-        h1 = h2;
-        d03 = e03;
-        d47 = e47;
-      }
-    }
+    cocg_phase_a(P, s.act, c, row_begin, row_end, H, h, s_b, lpart, acc);
     if (!group_sync_reduce<kCND, 6>(X, sh, acc, g, c)) return;
     ++lockstep;
     if (s.act) {
@@ -667,6 +696,7 @@ struct SpectralState {
   double* jout = nullptr;
   double* coef = nullptr;  // [N][nterms] excitation at T_sub per row
   int idft_blocks = 0;
+  bool warm_valid = false;  // x holds the last successful solve's solution (warm-start value)
   cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 
@@ -892,6 +922,9 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
   const int N = s->N, d = s->d, H = s->H;
   cudaEventRecord(s->e0, st);
   const double* rhs = rhs_il ? rhs_il : s->rhs;
+  // warm start (ps_krylov_settings.warm_start): from the last successful solve
+  const bool warm = cocg.warm_start != 0 && s->warm_valid;
+  s->warm_valid = false;
   int64_t lock_total = 0, its_total = 0;
   int max_its = 0;
   if (H > 0) {
@@ -931,6 +964,7 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
     P.q = s->q;
     P.tol = cocg.tol_rel;
     P.max_iter = cocg.max_iter;
+    P.warm = warm ? 1 : 0;
     P.sync = s->sync;
     P.partials = s->partials;
     P.abort_flag = s->abort_flag;
@@ -1016,9 +1050,11 @@ int spectral_solve(SpectralState* s, const DevProblem& p, const ps_krylov_settin
     for (int hh = 0; hh < H; ++hh) bytes += static_cast<double>(iters[hh]) * 160.0 * dd;
     bytes += static_cast<double>(lock_total) * (20.0 * nz + 4.0 * (dd + 1.0));
     bytes += 2.0 * (8.0 * N * dd + 16.0 * H * dd) + 8.0 * N * dd;
+    if (warm) bytes += H * 32.0 * dd + 20.0 * nz + 4.0 * (dd + 1.0);  // warm start: q = Lambda x once
     status->algorithmic_bytes = bytes;
     status->kernel_ms = ms;
   }
+  s->warm_valid = (rc == PS_OK && H > 0);
   return rc;
 }
 

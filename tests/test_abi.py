@@ -32,7 +32,9 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_abi.ps_problem_desc) == 144
     assert C.sizeof(_abi.ps_batch_status) == 72
     assert C.sizeof(_abi.ps_newton_settings) == 32
-    assert C.sizeof(_abi.ps_history) == 8 + 8 * 256 + 4 * 8 + 4 * 8 + 8 + 8  # + final_defect
+    # + final_defect, then the per-iteration COCG / fine / spectral arrays
+    assert C.sizeof(_abi.ps_history) == 8 + 8 * 256 + 4 * 8 + 4 * 8 + 8 + 8 + 3 * 8 * 256
+    assert C.sizeof(_abi.ps_krylov_settings) == 16
 
 
 def test_default_settings_are_reference_defaults():
