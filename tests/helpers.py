@@ -3,8 +3,8 @@ import numpy as np
 
 import paper_1905_13076_b200 as ps
 
-# BASELINE Newton / solver settings: Newton 1e-10 relative with an
-# absolute floor above the fp64 residual floor, opt-in backtracking.
+# BASELINE Newton / solver settings: Newton 1e-10 relative (BASELINE
+# configs[1]) with the reference's 1e-9 absolute floor, opt-in backtracking.
 NEWTON_BASELINE = ps.NewtonSettings(tol_abs=1e-9, tol_rel=1e-10, max_iter=50, line_search=30)
 
 

@@ -24,8 +24,10 @@ pytestmark = pytest.mark.gpu
 
 TOL = 1e-9
 SEED = 19051307
-# tools/current_bisect.py bisect 20 200 (profiles/r02_config0_current_bisect.jsonl)
-CONFIG0_CONVERGENT_CURRENT = float(os.environ.get("PPPC_CONFIG0_CURRENT", "50.0"))
+# tools/current_bisect.py bisect 20 2000 --steps 9 (oracle, direct LDL^T, 40 iterations;
+# profiles/r02_config0_current_bisect.jsonl): 74.2 A converges in 35 iterations, 78.1 A
+# not within 40, 143.8 A and above diverge
+CONFIG0_CONVERGENT_CURRENT = float(os.environ.get("PPPC_CONFIG0_CURRENT", "74.2"))
 
 
 def _config0(current):
