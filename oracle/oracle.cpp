@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <complex>
 #include <cstring>
 #include <exception>
@@ -674,6 +675,31 @@ void dft_bins(int n, int d, const cd* in, cd* out, int sign) {
     tw[k] = cd(std::cos(ang), sign < 0 ? -std::sin(ang) : std::sin(ang));
   }
   const double scale = 1.0 / std::sqrt(static_cast<double>(n));
+  if (n >= 64 && (n & (n - 1)) == 0) {
+    // large power-of-two block counts: iterative radix-2 FFT per DOF (the
+    // reference runs FFTW, proj/src/spectral.cpp:42-50), same unitary scale
+    int lg = 0;
+    while ((1 << lg) < n) ++lg;
+    std::vector<cd> a(n);
+    for (int j = 0; j < d; ++j) {
+      for (int m = 0; m < n; ++m) {
+        int r = 0;
+        for (int bit = 0; bit < lg; ++bit) r |= ((m >> bit) & 1) << (lg - 1 - bit);
+        a[r] = in[static_cast<int64_t>(m) * d + j];
+      }
+      for (int len = 2; len <= n; len <<= 1) {
+        const int half = len >> 1, step = n / len;
+        for (int i0 = 0; i0 < n; i0 += len)
+          for (int k = 0; k < half; ++k) {
+            const cd t = tw[static_cast<int64_t>(k) * step] * a[i0 + k + half];
+            a[i0 + k + half] = a[i0 + k] - t;
+            a[i0 + k] += t;
+          }
+      }
+      for (int b = 0; b < n; ++b) out[static_cast<int64_t>(b) * d + j] = scale * a[b];
+    }
+    return;
+  }
   for (int b = 0; b < n; ++b) {
     for (int j = 0; j < d; ++j) {
       cd acc(0.0, 0.0);
@@ -724,6 +750,11 @@ void assemble_rhs(const Problem& lin, const Mesh& mesh, const double* F, const d
   }
 }
 
+// per-bin factor / back-substitution seconds of the last DIRECT mh_solve (summed
+// over bins) and the wall seconds of its bin loop (or_last_direct_timing)
+std::mutex g_direct_timing_mu;
+double g_direct_timing[3] = {0.0, 0.0, 0.0};
+
 // MultiharmonicCyclicSolver (proj/src/spectral.cpp:224-279) with the bin mask
 // and shift-kind extensions of SURVEY.md App. A.3/A.4.
 // warm (ITERATIVE, s.cocg.warm_start): the previous solve's spectrum, used as
@@ -747,6 +778,8 @@ void mh_solve(const Problem& lin, const Mesh& mesh, const ps_solver_settings& s,
   dft_bins(n, d, in.data(), hat.data(), -1);
   const int last = conj ? n / 2 : n - 1;
   std::vector<int64_t> its(last + 1, 0);
+  if (mode == OR_DIRECT) g_direct_timing[0] = g_direct_timing[1] = 0.0;
+  const auto t_loop = std::chrono::steady_clock::now();
   parallel_for(last + 1, workers, [&](int bin) {
     if (mask && mask[bin] == 0) return;
     const int p = harmonic_index(bin, n);
@@ -761,14 +794,22 @@ void mh_solve(const Problem& lin, const Mesh& mesh, const ps_solver_settings& s,
     cd* x = &sol[static_cast<int64_t>(bin) * d];
     const cd* b = &hat[static_cast<int64_t>(bin) * d];
     if (mode == OR_DIRECT) {
+      // factor once per bin (the solver's constructor, proj/src/spectral.cpp:233-255),
+      // then the per-iteration back-substitution (:257-279); both timed per bin
+      const auto t0 = std::chrono::steady_clock::now();
       Ldlt<cd> f;
       f.factor(lin, [&](int64_t q) { return lam[q]; });
+      const auto t1 = std::chrono::steady_clock::now();
       if (!f.ok) {
         std::ostringstream msg;
         msg << "spectral: harmonic block p = " << p << " is singular";
         throw Error(PS_ERR_SINGULAR_BLOCK, msg.str());
       }
       f.solve(b, x);
+      const auto t2 = std::chrono::steady_clock::now();
+      std::lock_guard<std::mutex> lk(g_direct_timing_mu);
+      g_direct_timing[0] += std::chrono::duration<double>(t1 - t0).count();
+      g_direct_timing[1] += std::chrono::duration<double>(t2 - t1).count();
     } else {
       std::vector<cd> dinv(d);
       for (int i = 0; i < d; ++i) dinv[i] = cd(1.0, 0.0) / lam[lin.slot(i, i)];
@@ -795,6 +836,8 @@ void mh_solve(const Problem& lin, const Mesh& mesh, const ps_solver_settings& s,
       if (!std::isfinite(x[i].real()) || !std::isfinite(x[i].imag()))
         throw Error(PS_ERR_NONFINITE, "spectral: harmonic solve produced non-finite values");
   });
+  if (mode == OR_DIRECT)
+    g_direct_timing[2] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_loop).count();
   if (cocg_iters) *cocg_iters += std::accumulate(its.begin(), its.end(), int64_t{0});
   if (warm && s.cocg.warm_start && mode != OR_DIRECT) *warm = sol;
   if (conj)
@@ -997,6 +1040,14 @@ int or_mh_solve(const or_problem* lin, const ps_time_mesh* mesh, const ps_solver
     mh_solve(*lin->p, make_mesh(mesh), *s, mode, use_conjugate_symmetry != 0, bin_mask, shift_kind,
              rhs, U, workers, cocg_iterations);
   });
+}
+
+int or_last_direct_timing(double* factor_s, double* solve_s, double* wall_s) {
+  std::lock_guard<std::mutex> lk(g_direct_timing_mu);
+  if (factor_s) *factor_s = g_direct_timing[0];
+  if (solve_s) *solve_s = g_direct_timing[1];
+  if (wall_s) *wall_s = g_direct_timing[2];
+  return PS_OK;
 }
 
 // solve_cyclic_direct (proj/src/spectral.cpp:152-188): dense (N d)^2 Gaussian

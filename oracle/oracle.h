@@ -74,6 +74,9 @@ int or_forward_dft(int32_t n, int32_t d, const double* U, double* spectrum);
 int or_inverse_dft(int32_t n, int32_t d, const double* spectrum, double* U);
 int or_assemble_rhs(const or_problem* lin, const ps_time_mesh* mesh, const double* F,
                     const double* G, double* rhs);
+/* seconds of the last DIRECT or_mh_solve: per-bin factorizations and
+ * back-substitutions summed over bins, and the wall time of its bin loop */
+int or_last_direct_timing(double* factor_s, double* solve_s, double* wall_s);
 int or_mh_solve(const or_problem* lin, const ps_time_mesh* mesh, const ps_solver_settings* s,
                 int32_t mode, int32_t use_conjugate_symmetry, const int32_t* bin_mask,
                 int32_t shift_kind, const double* rhs, double* U, int32_t workers,

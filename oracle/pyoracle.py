@@ -60,6 +60,7 @@ _SIG = {
     "or_mh_solve": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh), C.POINTER(_abi.ps_solver_settings), C.c_int32,
                               C.c_int32, ip, C.c_int32, dp, dp, C.c_int32, C.POINTER(C.c_int64)]),
     "or_solve_cyclic_direct": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh), dp, dp]),
+    "or_last_direct_timing": (C.c_int, [dp, dp, dp]),
     "or_jump_norm": (C.c_double, [C.c_int32, C.c_int32, dp, dp]),
     "or_pppc_solve": (C.c_int, [vp, C.POINTER(_abi.ps_time_mesh), C.POINTER(_abi.ps_solver_settings),
                                 C.POINTER(_abi.ps_engine_settings), C.c_int32, dp, dp, dp,
@@ -277,6 +278,10 @@ class Oracle:
                                  None if mask is None else mask.ctypes.data_as(ip), shift_kind, _p(_f(rhs)),
                                  _p(out), workers or workers_default(), C.byref(its)))
         self.last_cocg_iterations = its.value
+        if mode == DIRECT:
+            f, sv, w = C.c_double(0), C.c_double(0), C.c_double(0)
+            lib().or_last_direct_timing(C.byref(f), C.byref(sv), C.byref(w))
+            self.last_direct_timing = dict(factor_s=f.value, solve_s=sv.value, wall_s=w.value)
         return out
 
     def solve_cyclic_direct(self, mesh, rhs):
