@@ -123,7 +123,11 @@ struct ps_ctx {
     double* A = nullptr;
     double* D = nullptr;
     double* AE = nullptr;
+    double* AT = nullptr;  // AE transposed [kEll][d] (system-per-block engine)
   };
+  // system-per-block engine buffers: contiguous state, per-system ELL values, hub values
+  double *sb_u = nullptr, *sb_A = nullptr, *sb_hub = nullptr;
+  size_t sb_u_len = 0, sb_A_len = 0, sb_hub_len = 0;
   std::map<double, StepMatrix> step_cache;
   SpectralState* spec = nullptr;
   int spec_N = 0;
@@ -340,6 +344,30 @@ void build_problem(ps_ctx* ctx, const ps_problem_desc* desc) {
     }
     P.ME = upload(me.data(), me.size(), "padded mass rows");
     P.KE = upload(ke.data(), ke.size(), "padded stiffness rows");
+    // system-per-block engine: the same padded rows transposed ([kEll][d]) and the
+    // padded columns; eligible when every row has <= kEll slots but at most one
+    int longer = 0, hub = -1;
+    for (int i = 0; i < P.d; ++i)
+      if (P.h_rp[i + 1] - P.h_rp[i] > kEll) ++longer, hub = i;
+    if (!P.linear && P.npe > 0 && longer <= 1) {
+      std::vector<int> cT(static_cast<size_t>(P.d) * kEll);
+      std::vector<double> mT(cT.size(), 0.0), kT(cT.size(), 0.0);
+      for (int i = 0; i < P.d; ++i) {
+        const int b = P.h_rp[i], len = P.h_rp[i + 1] - b;
+        for (int k = 0; k < kEll; ++k) {
+          const size_t t = static_cast<size_t>(k) * P.d + i;
+          const bool slot = len <= kEll && k < len;
+          cT[t] = slot ? P.h_ci[b + k] : i;
+          mT[t] = slot ? P.h_M[b + k] : 0.0;
+          kT[t] = slot ? Kref[b + k] : 0.0;
+        }
+      }
+      P.ciT = upload(cT.data(), cT.size(), "padded columns");
+      P.MT = upload(mT.data(), mT.size(), "padded mass columns");
+      P.KT = upload(kT.data(), kT.size(), "padded stiffness columns");
+      P.sb_ok = true;
+      P.sb_hub = hub;
+    }
   }
   P.nterms = desc->n_terms;
   P.period = desc->period;
@@ -446,6 +474,12 @@ ps_ctx::StepMatrix shared_step_matrix(ps_ctx* ctx, double dt) {
   m.A = upload(A.data(), A.size(), "step matrix");
   m.D = upload(D.data(), D.size(), "jacobi");
   m.AE = upload(AE.data(), AE.size(), "step matrix rows");
+  if (P.sb_ok) {
+    std::vector<double> AT(AE.size());
+    for (int i = 0; i < P.d; ++i)
+      for (int k = 0; k < kEll; ++k) AT[static_cast<size_t>(k) * P.d + i] = AE[static_cast<size_t>(i) * kEll + k];
+    m.AT = upload(AT.data(), AT.size(), "step matrix columns");
+  }
   return ctx->step_cache.emplace(dt, m).first->second;
 }
 
@@ -472,6 +506,24 @@ const char* failure_what(int code) {
 struct PropResult {
   double* state = nullptr;  // interleaved result (stride = count)
 };
+
+// Fine-propagation engine for a nonlinear element problem: the system-per-block
+// kernel (one block per system, block barriers only) or the lane kernel (one
+// warp lane per system, groups of blocks with device-wide group barriers).
+// PPPC_ENGINE=sys|lane forces one.  By default the system-per-block kernel runs
+// when the pattern qualifies (DevProblem::sb_ok) and a system's seven vectors
+// fit in one block's shared memory: small systems are latency-bound and gain
+// most from block barriers (configs[0], d = 2,497: fine sweep 9.8 -> 5.2 s per
+// 35 PP-PC iterations); at configs[1] size (d = 50,945) the lane kernel, which
+// reads the pattern and shared values once for 32 systems, is faster (25.8 s
+// against 34.5 s per step; profiles/r02_engines.log).
+bool use_sysblock(const ps_ctx* ctx, bool linear_path, bool probe_refill) {
+  if (linear_path || probe_refill || !ctx->P.sb_ok) return false;
+  static const char* env = std::getenv("PPPC_ENGINE");
+  if (env && std::strcmp(env, "lane") == 0) return false;
+  if (env && std::strcmp(env, "sys") == 0) return true;
+  return sysblock_smem(ctx->P.d) <= kSbSmemMax;
+}
 
 // Runs `steps` implicit-Euler steps of size dt for `count` systems whose
 // start states are in ctx->u (interleaved, stride count).  t_next is
@@ -610,7 +662,8 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   static const bool debug_timing = std::getenv("PPPC_DEBUG_TIMING") != nullptr;
   unsigned long long* dbg = nullptr;
   const int nblk = geo.G * geo.C;
-  if (debug_timing && dalloc(&dbg, static_cast<size_t>(nblk) * kDbgSlots)) K.dbg = dbg;
+  const bool sysblock = use_sysblock(ctx, linear_path, probe_refill);
+  if (debug_timing && !sysblock && dalloc(&dbg, static_cast<size_t>(nblk) * kDbgSlots)) K.dbg = dbg;
   // The SpMV gathers the search direction p at +-ntheta rows; keep p resident in
   // L2 (persisting access-policy window) so the streamed matrix values and
   // vectors do not evict it between neighbour reads.  PPPC_NO_L2_PERSIST=1 off.
@@ -636,7 +689,29 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   }
   check(cudaEventRecord(ctx->e0, ctx->stream), "event");
   std::string err;
-  if (sequential_groups() && geo.G > 1) {
+  if (sysblock) {
+    ensure(&ctx->sb_u, &ctx->sb_u_len, static_cast<size_t>(count) * P.d);
+    ensure(&ctx->sb_A, &ctx->sb_A_len, static_cast<size_t>(count) * kEll * P.d);
+    SysParams sp{};
+    sp.su = ctx->sb_u;
+    sp.sA = ctx->sb_A;
+    sp.hub = P.sb_hub;
+    sp.hub_len = P.sb_hub >= 0 ? P.h_rp[P.sb_hub + 1] - P.h_rp[P.sb_hub] : 0;
+    if (sp.hub >= 0) {
+      ensure(&ctx->sb_hub, &ctx->sb_hub_len, static_cast<size_t>(count) * sp.hub_len);
+      sp.hubA = ctx->sb_hub;
+    }
+    sp.ciT = P.ciT;
+    sp.MT = P.MT;
+    sp.KT = P.KT;
+    sp.AshT = shared_step_matrix(ctx, dt).AT;
+    static const bool no_smem = std::getenv("PPPC_SB_NO_SMEM") != nullptr;
+    sp.smem_vectors = (!no_smem && sysblock_smem(P.d) <= kSbSmemMax) ? 1 : 0;
+    check(cudaMemsetAsync(ctx->lockstep, 0, geo.G * sizeof(int64_t), ctx->stream), "lockstep reset");
+    check(cudaEventRecord(ctx->e0, ctx->stream), "event");
+    const int rc = launch_sysblock(K, sp, npe, ctx->stream, &err);
+    if (rc != PS_OK) throw Failure(rc, err);
+  } else if (sequential_groups() && geo.G > 1) {
     // one launch per group, each on all C blocks, own arrival counter
     for (int gg = 0; gg < geo.G; ++gg) {
       PropParams Kg = K;
@@ -934,7 +1009,11 @@ void ps_destroy(ps_ctx* ctx) {
     cudaFree(kv.second.A);
     cudaFree(kv.second.D);
     cudaFree(kv.second.AE);
+    if (kv.second.AT) cudaFree(kv.second.AT);
   }
+  void* sb[] = {P.ciT, P.MT, P.KT, ctx->sb_u, ctx->sb_A, ctx->sb_hub};
+  for (void* q : sb)
+    if (q) cudaFree(q);
   if (ctx->spec) spectral_free(ctx->spec);
   if (ctx->e0) cudaEventDestroy(ctx->e0);
   if (ctx->e1) cudaEventDestroy(ctx->e1);

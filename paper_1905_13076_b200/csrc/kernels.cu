@@ -1118,6 +1118,504 @@ __global__ void __launch_bounds__(kThreads, 1) propagate_kernel(const PropParams
     for (int k = 0; k < kDbgSlots; ++k) P.dbg[static_cast<size_t>(blockIdx.x) * kDbgSlots + k] = dbg[k];
 }
 
+// ------------------------------------------------- system-per-block engine
+// One thread block runs one system's whole batch of implicit-Euler steps
+// (proj/src/propagators.cpp:96-115): the refill, the Newton control
+// (:27-58, with the same backtracking extension as propagate_kernel) and every
+// Jacobi-PCG iteration, synchronising with block barriers only.  Vectors are
+// contiguous per system and thread t owns rows t, t + NT, ..., so every
+// operand of a row (the padded ELL column list, the shared or per-system slot
+// values, the gathered p entries of neighbouring rows) is a coalesced load
+// across a warp.  Same arithmetic and control flow as propagate_kernel's lane
+// state machine; block reductions run in a fixed order, so a system's result
+// does not depend on the batch it is in.
+
+// Fixed-order block sum of ND values: shuffle-down tree per warp, then the
+// warp partials in warp order.  Every thread returns the same totals.
+template <int ND, int NT>
+__device__ __forceinline__ void sb_reduce(double (&v)[ND], double (*red)[NT / 32], double* tot) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < ND; ++k) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < ND; ++k) red[k][warp] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < ND) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += red[threadIdx.x][w];
+    tot[threadIdx.x] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < ND; ++k) v[k] = tot[k];
+}
+
+struct SbVec {
+  double *u, *uprev, *x, *r, *p, *q, *D, *A, *hA;
+};
+
+__device__ __forceinline__ bool sb_shared_row(const PropParams& P, int i) {
+  return P.rowkind == nullptr || __ldg(P.rowkind + i) == 0;
+}
+
+// Refill of one row of <= kEll slots (refill_row_ell's arithmetic, contiguous
+// layout): excitation, residual R = M(u - u_prev)/dt + K(u)u - f, the step
+// matrix values M/dt + J(u) (per-system rows), Jacobi, r = -R, p = Dinv r;
+// partials {R.R, f.f, r.z, r.r}.
+template <int NPE>
+__device__ __forceinline__ void sb_refill_row(const PropParams& P, const SysParams& S, const ps_curve* curves,
+                                              const SbVec& V, int sys, int step, bool first, int i,
+                                              double (&acc)[4]) {
+  const int d = P.d;
+  const int base = __ldg(P.rp + i), len = __ldg(P.rp + i + 1) - base;
+  const bool shared_row = sb_shared_row(P, i);
+  int c[kEll];
+  double uc[kEll], upc[kEll], mv[kEll];
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) c[k] = __ldg(S.ciT + static_cast<size_t>(k) * d + i);
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) uc[k] = V.u[c[k]];
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) upc[k] = first ? 0.0 : V.uprev[c[k]];
+#pragma unroll
+  for (int k = 0; k < kEll; ++k) mv[k] = __ldg(S.MT + static_cast<size_t>(k) * d + i);
+  double mr = 0.0;
+  if (!first) {
+#pragma unroll
+    for (int k = 0; k < kEll; ++k)
+      if (k < len) mr += mv[k] * ((uc[k] - upc[k]) / P.dt);
+  }
+  double ku = 0.0, dinv;
+  if (shared_row) {
+#pragma unroll
+    for (int k = 0; k < kEll; ++k)
+      if (k < len) ku += __ldg(S.KT + static_cast<size_t>(k) * d + i) * uc[k];
+    dinv = __ldg(P.Dsh + i);
+  } else {
+    double jv[kEll];
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) jv[k] = 0.0;
+    const int q0 = __ldg(P.adj_ptr + i), q1 = __ldg(P.adj_ptr + i + 1);
+    for (int q = q0; q < q1; ++q) {
+      const int2 ea = __ldg(P.adj + q);
+      const int e = ea.x;
+      int rel[NPE];
+      Elem<NPE> E;
+#pragma unroll
+      for (int b = 0; b < NPE; ++b) {
+        rel[b] = __ldg(P.adj_rel + static_cast<size_t>(q) * NPE + b);
+        double ub = 0.0;
+#pragma unroll
+        for (int s = 0; s < kEll; ++s) ub = (rel[b] == s) ? uc[s] : ub;
+        E.ue[b] = ub;
+      }
+#pragma unroll
+      for (int k = 0; k < NPE * NPE; ++k) E.S[k] = __ldg(P.eS + static_cast<size_t>(e) * NPE * NPE + k);
+      double b2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < NPE; ++a) {
+        double sg = 0.0;
+#pragma unroll
+        for (int b = 0; b < NPE; ++b) sg += E.S[a * NPE + b] * E.ue[b];
+        E.g[a] = sg;
+        b2 += E.ue[a] * sg;
+      }
+      const double inva = __ldg(P.einvA + e);
+      b2 *= inva;
+      double nup;
+      curve_eval(curves[__ldg(P.ecurve + e)], b2, E.nu, nup);
+      E.cc = 2.0 * nup * inva;
+      double ga, Sa[NPE];
+      elem_row<NPE>(E, ea.y, ga, Sa);
+      ku += E.nu * ga;
+#pragma unroll
+      for (int b = 0; b < NPE; ++b) {
+        if (rel[b] < 0) continue;
+        const double v = E.nu * Sa[b] + E.cc * (ga * E.g[b]);
+#pragma unroll
+        for (int sl = 0; sl < kEll; ++sl) jv[sl] += (rel[b] == sl) ? v : 0.0;
+      }
+    }
+    double dval = 0.0;
+    const int dslot = __ldg(P.diag + i) - base;
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) {
+      // pad slots hold 0 (the SpMV reads all kEll slots of a row)
+      const double av = k < len ? mv[k] / P.dt + jv[k] : 0.0;
+      V.A[static_cast<size_t>(k) * d + i] = av;
+      if (k == dslot) dval = av;
+    }
+    dinv = 1.0 / dval;
+    V.D[i] = dinv;
+  }
+  double f = 0.0;
+  const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
+  for (int t = 0; t < P.nterms; ++t) f += __ldg(cf + t) * __ldg(P.pat + static_cast<size_t>(t) * d + i);
+  const double R = mr + ku - f;
+  const double r = -R;
+  const double z = dinv * r;
+  V.r[i] = r;
+  V.p[i] = z;
+  if (first) V.uprev[i] = V.u[i];
+  acc[0] += R * R;
+  acc[1] += f * f;
+  acc[2] += r * z;
+  acc[3] += r * r;
+}
+
+// The hub row (more than kEll slots), serially by one thread: refill_row's
+// arithmetic on the CSR slots.
+template <int NPE>
+__device__ void sb_refill_hub(const PropParams& P, const SysParams& S, const ps_curve* curves, const SbVec& V,
+                              int sys, int step, bool first, double (&acc)[4]) {
+  const int i = S.hub, d = P.d;
+  const int base = __ldg(P.rp + i), end = __ldg(P.rp + i + 1);
+  const bool shared_row = sb_shared_row(P, i);
+  double ku = 0.0;
+  if (shared_row) {
+    for (int k = base; k < end; ++k) ku += __ldg(P.Kc + k) * V.u[__ldg(P.ci + k)];
+  } else {
+    for (int k = 0; k < end - base; ++k) V.hA[k] = 0.0;
+    const int q0 = __ldg(P.adj_ptr + i), q1 = __ldg(P.adj_ptr + i + 1);
+    for (int q = q0; q < q1; ++q) {
+      const int2 ea = __ldg(P.adj + q);
+      Elem<NPE> E;
+      eval_elem<NPE>(P, curves, ea.x, V.u, 0, 1, E);
+      double ga, Sa[NPE];
+      elem_row<NPE>(E, ea.y, ga, Sa);
+      ku += E.nu * ga;
+#pragma unroll
+      for (int b = 0; b < NPE; ++b) {
+        const int rel = __ldg(P.adj_rel + static_cast<size_t>(q) * NPE + b);
+        if (rel < 0) continue;
+        V.hA[rel] += E.nu * Sa[b] + E.cc * (ga * E.g[b]);
+      }
+    }
+  }
+  double mr = 0.0, dval = 0.0;
+  const int dslot = __ldg(P.diag + i);
+  for (int k = base; k < end; ++k) {
+    const double mk = __ldg(P.M + k);
+    if (!first) {
+      const int j = __ldg(P.ci + k);
+      mr += mk * ((V.u[j] - V.uprev[j]) / P.dt);
+    }
+    if (shared_row) continue;
+    const double av = mk / P.dt + V.hA[k - base];
+    V.hA[k - base] = av;
+    if (k == dslot) dval = av;
+  }
+  double f = 0.0;
+  const double* cf = P.coef + (static_cast<size_t>(step) * P.count + sys) * P.nterms;
+  for (int t = 0; t < P.nterms; ++t) f += __ldg(cf + t) * __ldg(P.pat + static_cast<size_t>(t) * d + i);
+  const double dinv = shared_row ? __ldg(P.Dsh + i) : 1.0 / dval;
+  const double R = mr + ku - f;
+  const double r = -R;
+  const double z = dinv * r;
+  if (!shared_row) V.D[i] = dinv;
+  V.r[i] = r;
+  V.p[i] = z;
+  if (first) V.uprev[i] = V.u[i];
+  acc[0] += R * R;
+  acc[1] += f * f;
+  acc[2] += r * z;
+  acc[3] += r * r;
+}
+
+template <int NPE, int NT>
+__device__ __forceinline__ void sb_refill(const PropParams& P, const SysParams& S, const ps_curve* curves,
+                                          const SbVec& V, int sys, int step, bool first, double (*red)[NT / 32],
+                                          double* tot, double (&t)[4]) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int i = threadIdx.x; i < P.d; i += NT)
+    if (i != S.hub) sb_refill_row<NPE>(P, S, curves, V, sys, step, first, i, acc);
+  // the hub row serially on the last thread (it owns the fewest rows)
+  if (S.hub >= 0 && threadIdx.x == NT - 1) sb_refill_hub<NPE>(P, S, curves, V, sys, step, first, acc);
+  sb_reduce<4, NT>(acc, red, tot);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) t[k] = acc[k];
+}
+
+// Phase A over this thread's rows, two rows per round with all their loads
+// issued before the first FMA: q = A p and the partials p.q, q.z, q.Dq.  The
+// hub row is skipped (its product goes through the reduction).
+template <int NT>
+__device__ __forceinline__ void sb_spmv_rows(const PropParams& P, const SysParams& S, const SbVec& V,
+                                             double (&acc)[4]) {
+  const int d = P.d;
+  for (int i0 = threadIdx.x; i0 < d; i0 += 2 * NT) {
+    int row[2] = {i0, i0 + NT};
+    bool ok[2] = {i0 != S.hub, i0 + NT < d && i0 + NT != S.hub};
+    double av[2][kEll], pv[2][kEll], po[2], ro[2], dv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = ok[u] ? row[u] : i0;  // a skipped row re-reads row i0 (results unused)
+      // shared and per-system operands are both requested and then selected by
+      // the row kind, so no load waits on the kind
+      const bool sh = sb_shared_row(P, i);
+      double as[kEll], ap[kEll];
+#pragma unroll
+      for (int k = 0; k < kEll; ++k) {
+        const size_t t = static_cast<size_t>(k) * d + i;
+        as[k] = __ldg(S.AshT + t);
+        ap[k] = V.A[t];
+        pv[u][k] = V.p[__ldg(S.ciT + t)];
+      }
+#pragma unroll
+      for (int k = 0; k < kEll; ++k) av[u][k] = sh ? as[k] : ap[k];
+      po[u] = V.p[i];
+      ro[u] = V.r[i];
+      const double ds = __ldg(P.Dsh + i), dp = V.D[i];
+      dv[u] = sh ? ds : dp;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      double qv = 0.0;
+#pragma unroll
+      for (int k = 0; k < kEll; ++k) qv += av[u][k] * pv[u][k];
+      V.q[row[u]] = qv;
+      const double zi = dv[u] * ro[u];
+      acc[0] += po[u] * qv;
+      acc[1] += qv * zi;
+      acc[2] += qv * (dv[u] * qv);
+    }
+  }
+}
+
+// Phase B over this thread's rows, two rows per round: x (+)= alpha p,
+// r -= alpha q, z = D r, p = z + beta p; partials r.r, r.z.
+template <int NT>
+__device__ __forceinline__ void sb_update_rows(const PropParams& P, const SbVec& V, double alpha, double beta,
+                                               bool first, double (&acc)[2]) {
+  const int d = P.d;
+  for (int i0 = threadIdx.x; i0 < d; i0 += 2 * NT) {
+    const int i1 = i0 + NT < d ? i0 + NT : i0;
+    const int row[2] = {i0, i1};
+    double dv[2], pv[2], xv[2], rv[2], qv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = row[u];
+      const double ds = __ldg(P.Dsh + i), dp = V.D[i];
+      dv[u] = sb_shared_row(P, i) ? ds : dp;
+      pv[u] = V.p[i];
+      xv[u] = first ? 0.0 : V.x[i];
+      rv[u] = V.r[i];
+      qv[u] = V.q[i];
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (u == 1 && i0 + NT >= d) break;
+      const int i = row[u];
+      V.x[i] = first ? alpha * pv[u] : xv[u] + alpha * pv[u];
+      const double rn = rv[u] - alpha * qv[u];
+      const double z = dv[u] * rn;
+      V.r[i] = rn;
+      V.p[i] = z + beta * pv[u];
+      acc[0] += rn * rn;
+      acc[1] += rn * z;
+    }
+  }
+}
+
+template <int NPE, int NT>
+__global__ void __launch_bounds__(NT, 1) sysblock_kernel(const PropParams P, const SysParams S) {
+  __shared__ double red[4][NT / 32];
+  __shared__ double tot[4];
+  __shared__ ps_curve curves[kMaxCurves];
+  const int sys = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid < P.ncurves) curves[tid] = P.curves[tid];
+  const int d = P.d;
+  const size_t vb = static_cast<size_t>(sys) * d;
+  SbVec V;
+  if (S.smem_vectors) {
+    // small systems: the seven per-row vectors live in shared memory
+    extern __shared__ __align__(16) double sv[];
+    V.u = sv;
+    V.uprev = sv + d;
+    V.x = sv + 2 * static_cast<size_t>(d);
+    V.r = sv + 3 * static_cast<size_t>(d);
+    V.p = sv + 4 * static_cast<size_t>(d);
+    V.q = sv + 5 * static_cast<size_t>(d);
+    V.D = sv + 6 * static_cast<size_t>(d);
+  } else {
+    V.u = S.su + vb;
+    V.uprev = P.uprev + vb;
+    V.x = P.x + vb;
+    V.r = P.r + vb;
+    V.p = P.p + vb;
+    V.q = P.q + vb;
+    V.D = P.Dinv + vb;
+  }
+  V.A = S.sA + static_cast<size_t>(sys) * kEll * d;
+  V.hA = S.hub >= 0 ? S.hubA + static_cast<size_t>(sys) * S.hub_len : nullptr;
+  // start state from the group-blocked layout [G][d][32] (the callers' staging)
+  const int g = sys / P.L, l = sys - g * P.L;
+  double* ub = P.u + static_cast<size_t>(g) * d * kLanes + l;
+  for (int i = tid; i < d; i += NT) V.u[i] = ub[static_cast<size_t>(i) * kLanes];
+  __syncthreads();
+
+  const bool hub_shared = S.hub >= 0 && sb_shared_row(P, S.hub);
+  const int hub_base = S.hub >= 0 ? __ldg(P.rp + S.hub) : 0;
+  int code = PS_OK, last_nit = 0, max_nit = 0, max_pit = 0;
+  double t_fail = 0.0, res_fail = 0.0;
+  long long newton_total = 0, pcg_total = 0;
+  double t[4];
+  for (int step = 0; step < P.steps && code == PS_OK; ++step) {
+    const double t_now = P.t_next[static_cast<size_t>(step) * P.count + sys];
+    sb_refill<NPE, NT>(P, S, curves, V, sys, step, true, red, tot, t);
+    const double tol = P.newton_tol_abs + P.newton_tol_rel * sqrt(t[1]);
+    int nit = 1;
+    double res_pre = sqrt(t[0]);
+    double rho = t[2], bb = t[3];
+    for (;;) {
+      // ---- step solve (J delta = -R): Jacobi-PCG from delta = 0
+      const bool pact = bb != 0.0;
+      if (pact) {
+        const double stop = (P.pcg_tol * P.pcg_tol) * bb;
+        int pit = 0;
+        for (;;) {
+          double a4[4] = {0.0, 0.0, 0.0, 0.0};
+          sb_spmv_rows<NT>(P, S, V, a4);
+          if (S.hub >= 0) {
+            double part = 0.0;
+            for (int s = tid; s < S.hub_len; s += NT) {
+              const int k = hub_base + s;
+              const double av = hub_shared ? __ldg(P.Ash + k) : V.hA[s];
+              part += av * V.p[__ldg(P.ci + k)];
+            }
+            a4[3] = part;
+          }
+          sb_reduce<4, NT>(a4, red, tot);
+          double t0v = a4[0], t1v = a4[1], t2v = a4[2];
+          if (S.hub >= 0) {
+            // the hub's q came through the reduction: its terms are added to the
+            // dots here (uniformly), its owner stores it for the update
+            const double qh = a4[3], ph = V.p[S.hub], rh = V.r[S.hub];
+            const double dh = hub_shared ? __ldg(P.Dsh + S.hub) : V.D[S.hub];
+            t0v += ph * qh;
+            t1v += qh * (dh * rh);
+            t2v += qh * (dh * qh);
+            if (tid == S.hub % NT) V.q[S.hub] = qh;
+          }
+          if (!isfinite(t0v) || t0v == 0.0) {
+            code = PS_ERR_SINGULAR;
+            res_fail = res_pre;
+            t_fail = t_now;
+            break;
+          }
+          const double alpha = rho / t0v;
+          const double rho_est = rho - 2.0 * alpha * t1v + alpha * alpha * t2v;
+          const double beta = rho_est / rho;
+          double b2[2] = {0.0, 0.0};
+          sb_update_rows<NT>(P, V, alpha, beta, pit == 0, b2);
+          sb_reduce<2, NT>(b2, red, tot);
+          const double rr = b2[0];
+          rho = b2[1];
+          pit += 1;
+          if (rr <= stop) break;
+          if (!isfinite(rr)) {
+            code = PS_ERR_SINGULAR;
+            res_fail = res_pre;
+            t_fail = t_now;
+            break;
+          }
+          if (pit >= P.pcg_max) {
+            code = PS_ERR_PCG_MAXITER;
+            res_fail = res_pre;
+            t_fail = t_now;
+            break;
+          }
+        }
+        if (code != PS_OK) break;
+        pcg_total += pit;
+        max_pit = max(max_pit, pit);
+      }
+      // ---- trial update u += lambda delta (propagators.cpp:46-48), delta finite
+      double lambda = P.damping;
+      int ls_k = 0;
+      if (pact) {
+        double bad[1] = {0.0};
+        for (int i = tid; i < d; i += NT) {
+          const double dx = V.x[i];
+          bad[0] += isfinite(dx) ? 0.0 : 1.0;
+          V.u[i] += lambda * dx;
+        }
+        sb_reduce<1, NT>(bad, red, tot);
+        if (bad[0] > 0.0) {
+          code = PS_ERR_SINGULAR;
+          res_fail = res_pre;
+          t_fail = t_now;
+          break;
+        }
+      } else {
+        __syncthreads();
+      }
+      // ---- residual at the trial point; optional backtracking
+      double post;
+      for (;;) {
+        sb_refill<NPE, NT>(P, S, curves, V, sys, step, false, red, tot, t);
+        post = sqrt(t[0]);
+        if (P.line_search > 0 && ls_k < P.line_search && !(post <= tol) &&
+            !(post <= (1.0 - 1e-4 * lambda) * res_pre)) {
+          lambda *= 0.5;
+          ls_k += 1;
+          if (pact)
+            for (int i = tid; i < d; i += NT) V.u[i] -= lambda * V.x[i];
+          __syncthreads();
+          continue;
+        }
+        break;
+      }
+      if (tid == 0 && P.trace) P.trace[static_cast<size_t>(sys) * P.newton_max + (nit - 1)] = post;
+      if (!isfinite(post)) {
+        code = PS_ERR_NEWTON_DIVERGED;
+        res_fail = post;
+        t_fail = t_now;
+        break;
+      }
+      if (post <= tol) {
+        newton_total += nit;
+        last_nit = nit;
+        max_nit = max(max_nit, nit);
+        break;
+      }
+      if (nit >= P.newton_max) {
+        code = PS_ERR_NEWTON_MAXITER;
+        res_fail = post;
+        t_fail = t_now;
+        break;
+      }
+      nit += 1;
+      res_pre = post;
+      rho = t[2];
+      bb = t[3];
+    }
+  }
+  // result back to the group-blocked layout
+  for (int i = tid; i < d; i += NT) ub[static_cast<size_t>(i) * kLanes] = V.u[i];
+  if (tid == 0) {
+    SysOut o;
+    o.code = code;
+    o.newton_last = last_nit;
+    o.t_fail = t_fail;
+    o.residual = res_fail;
+    o.newton_total = newton_total;
+    o.pcg_total = pcg_total;
+    o.max_newton = max_nit;
+    o.max_pcg = max_pit;
+    P.out[sys] = o;
+    atomicMax(reinterpret_cast<unsigned long long*>(P.lockstep + g), static_cast<unsigned long long>(pcg_total));
+  }
+}
+
 // ------------------------------------------------------- phase probes
 // One PCG phase over the whole batch with the propagation kernel's exact thread
 // -> (group, row, lane) mapping and code, but no barriers or state machine:
@@ -1388,6 +1886,35 @@ void launch_axpby_shared(const double* a, double sa, const double* b, double sb,
 void launch_eval_curve(const ps_curve& c, int n, const double* b2, double* nu, double* nup, cudaStream_t st) {
   if (n <= 0) return;
   curve_kernel<<<(n + 255) / 256, 256, 0, st>>>(c, n, b2, nu, nup);
+}
+
+#ifndef PPPC_SB_THREADS
+#define PPPC_SB_THREADS 512
+#endif
+constexpr int kSbThreads = PPPC_SB_THREADS;
+
+size_t sysblock_smem(int d) { return static_cast<size_t>(7) * d * sizeof(double); }
+
+int launch_sysblock(const PropParams& prm, const SysParams& sp, int npe, cudaStream_t st, std::string* err) {
+  const size_t smem = sp.smem_vectors ? sysblock_smem(prm.d) : 0;
+  void* fn = npe == 2 ? reinterpret_cast<void*>(&sysblock_kernel<2, kSbThreads>)
+                      : reinterpret_cast<void*>(&sysblock_kernel<3, kSbThreads>);
+  if (npe != 2 && npe != 3) return PS_ERR_BAD_ARG;
+  if (smem > 0 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+                      cudaSuccess) {
+    if (err) *err = "cuda: sysblock shared-memory opt-in failed";
+    return PS_ERR_CUDA;
+  }
+  if (npe == 2)
+    sysblock_kernel<2, kSbThreads><<<prm.count, kSbThreads, smem, st>>>(prm, sp);
+  else
+    sysblock_kernel<3, kSbThreads><<<prm.count, kSbThreads, smem, st>>>(prm, sp);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (err) *err = std::string("cuda: sysblock launch failed: ") + cudaGetErrorString(e);
+    return PS_ERR_CUDA;
+  }
+  return PS_OK;
 }
 
 int launch_phase_probe(const PropParams& prm, int mode, double* sink, cudaStream_t st) {

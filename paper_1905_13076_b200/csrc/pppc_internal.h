@@ -121,6 +121,25 @@ struct PropParams {
 
 struct DftPlan;
 
+// System-per-block engine (kernels.cu sysblock_kernel): one thread block runs
+// one system's whole propagation (every step, Newton iteration and PCG
+// iteration) with block barriers only; per-system vectors are contiguous
+// ([count][d], thread = row), so the SpMV gathers are coalesced across rows.
+struct SysParams {
+  double* su;           // state u [count][d] (the start state is gathered from P.u, group-blocked)
+  double* sA;           // per-system step-matrix values of rows <= kEll slots, ELL [count][kEll][d]
+  double* hubA;         // per-system values of the hub row [count][hub_len] (rows > kEll slots: at most one)
+  const int* ciT;       // [kEll][d] padded ELL columns (pad = the row itself)
+  const double* MT;     // [kEll][d] padded mass values
+  const double* KT;     // [kEll][d] padded shared stiffness values (K_const)
+  const double* AshT;   // [kEll][d] padded shared step-matrix values M/dt + K_const (per dt)
+  int hub;              // the row longer than kEll, or -1
+  int hub_len;
+  int smem_vectors;     // 1: u, u_prev, x, r, p, q, Dinv in shared memory (7 d doubles)
+};
+size_t sysblock_smem(int d);
+constexpr size_t kSbSmemMax = 200 * 1024;
+
 // Device-resident problem + work buffers owned by a context.
 struct DevProblem {
   int d = 0, nnz = 0;
@@ -154,6 +173,13 @@ struct DevProblem {
   // element problems: rows touching only constant-nu elements share their values
   unsigned char* rowkind = nullptr;
   double* Kc = nullptr;
+  // system-per-block engine: transposed padded rows; sb_ok = the pattern qualifies
+  // (every row <= kEll slots but at most one longer row)
+  bool sb_ok = false;
+  int sb_hub = -1;
+  int* ciT = nullptr;
+  double* MT = nullptr;
+  double* KT = nullptr;
   std::vector<unsigned char> h_rowkind;
   std::vector<double> h_Kc;
 };
@@ -182,6 +208,7 @@ void launch_eval_curve(const ps_curve& c, int n, const double* b2, double* nu, d
                        cudaStream_t st);
 void launch_frozen_K(const DevProblem& p, const double* u_ref, double* K_out, cudaStream_t st);
 int launch_phase_probe(const PropParams& prm, int mode, double* sink, cudaStream_t st);
+int launch_sysblock(const PropParams& prm, const SysParams& sp, int npe, cudaStream_t st, std::string* err);
 
 // spectral (spectral.cu)
 struct SpectralState;
