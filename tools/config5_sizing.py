@@ -33,6 +33,9 @@ ap.add_argument("--N", type=int, nargs="*", default=[16, 64, 256])
 ap.add_argument("--nr", type=int, default=2000)
 ap.add_argument("--ntheta", type=int, default=2048)
 ap.add_argument("--pcg-tol", type=float, default=1e-2)
+ap.add_argument("--pcg-max", type=int, default=5000)
+ap.add_argument("--newton-max", type=int, default=1, help="1: one Newton iteration (stops with 'did not converge')")
+ap.add_argument("--no-probes", action="store_true")
 a = ap.parse_args()
 
 t0 = time.perf_counter()
@@ -48,9 +51,10 @@ except Exception:
 for N in a.N:
     torch.cuda.synchronize()
     mesh = ps.TimeMesh(N, 10, prob.period)
-    newton = ps.NewtonSettings(tol_abs=1e-9, tol_rel=1e-10, max_iter=1, line_search=0)
+    newton = ps.NewtonSettings(tol_abs=1e-9, tol_rel=1e-10, max_iter=a.newton_max,
+                               line_search=0 if a.newton_max == 1 else 30)
     prop = ps.Propagator(prob, ps.TimeMesh(N * 10, 1, prob.period), newton,
-                         ps.KrylovSettings(tol_rel=a.pcg_tol, max_iter=5000), max_batch=N)
+                         ps.KrylovSettings(tol_rel=a.pcg_tol, max_iter=a.pcg_max), max_batch=N)
     g = torch.Generator(device=dev)
     g.manual_seed(19051307 + N)
     U = torch.randn((N, d), generator=g, device=dev, dtype=torch.float64) * 1e-3
@@ -65,19 +69,24 @@ for N in a.N:
     wall = time.perf_counter() - t1
     free, total = torch.cuda.mem_get_info(dev)
     probes = {}
-    for mode in (1, 2, 3):
+    for mode in (() if a.no_probes else (1, 2, 3)):
         ms, by = C.c_double(0), C.c_double(0)
         prop._check(ps.lib().ps_phase_probe(prop._ctx, mode, 3, C.byref(ms), C.byref(by)))
         probes[f"mode{mode}"] = {"us": ms.value * 1e3, "GBps": by.value / (ms.value / 1e3) / 1e9,
                                  "frac": by.value / (ms.value / 1e3) / 1e9 / peak}
-    line = {"measurement": "BASELINE configs[4] sizing (bounded: one Newton iteration of one step, PCG relaxed)",
+    what = ("one Newton iteration of the first fine step" if a.newton_max == 1 else
+            f"the first fine step (Newton <= {a.newton_max} iterations)")
+    line = {"measurement": f"BASELINE configs[4]: {what}, PCG rel {a.pcg_tol}",
             "nr": a.nr, "ntheta": a.ntheta, "dof": d, "nnz": prob.nnz, "N": N, "build_s": build_s,
             "device_used_GB": (total - free) / 1e9, "device_total_GB": total / 1e9,
             "step_wall_s": wall, "kernel_ms": st.kernel_ms, "newton_iterations": st.newton_iterations,
             "pcg_iterations": st.pcg_iterations, "pcg_tol": a.pcg_tol,
             "algorithmic_GBps": st.algorithmic_bytes / (st.kernel_ms / 1e3) / 1e9,
             "frac": st.algorithmic_bytes / (st.kernel_ms / 1e3) / 1e9 / peak, "phase_probes": probes,
-            "status": st.code}
+            "status": st.code, "max_pcg_per_solve": st.max_pcg_iterations,
+            "max_newton": st.max_newton_iterations, "newton_max": a.newton_max,
+            "dof_timesteps_per_s": (N * d / (st.kernel_ms / 1e3)) if a.newton_max > 1 and st.code == 0 else None,
+            "failed_residual": st.residual if st.code else None}
     print(json.dumps(line), flush=True)
     prop.close()
     del U, out
