@@ -280,10 +280,12 @@ def run_reference(args):
     """bench.py --impl reference: the reference's CPU algorithm (the oracle port;
     the reference itself cannot be built here) on the host cores.
     Problem and start values come from the oracle's own builder and generators,
-    so this process never loads libpppc_b200.so.  Each timed step is one fine
-    step of `cores` subintervals (CpuSampler), consecutive steps continuing the
-    same trajectories; warm-up steps propagate one subinterval by one fine step
-    (a CPU code has nothing to warm beyond page-in)."""
+    so this process never loads libpppc_b200.so.  Each timed step propagates
+    `cores` subintervals (one per core) over ALL s fine steps of their
+    subinterval (CpuSampler), the next step the next `cores` subintervals, so the
+    expensive first fine steps from the random start and the cheap later ones
+    are sampled in their true proportion; warm-up steps propagate one
+    subinterval by one fine step (a CPU code has nothing to warm beyond page-in)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -297,16 +299,17 @@ def run_reference(args):
     smp = CpuSampler(po, orc, mesh, newton, pcg, U, systems)
     el = units = 0.0
     for _ in range(args.steps):
-        e, u = smp.advance()
-        el += e
-        units += u
+        for _ in range(mesh.fine_steps):
+            e, u = smp.advance()
+            el += e
+            units += u
     value = units / el
     maps = open("/proc/self/maps").read()
     cb = {"value": value, "unit": UNIT, "cores": systems, "kind": "port",
-          "sample": f"per step: one fine step of {systems} subintervals (one per core), consecutive steps "
-                    f"continuing the same trajectories ({args.steps} steps = {args.steps / mesh.fine_steps:.2f} "
-                    f"x the s = {mesh.fine_steps} steps of a subinterval); direct LDL^T Newton (reference "
-                    f"algorithm, oracle built -march=native); {el:.1f} s",
+          "sample": f"per step: {systems} subintervals (one per core) over all {mesh.fine_steps} fine steps, "
+                    f"the next step the next {systems} subintervals ({args.steps * systems} of the "
+                    f"{mesh.subintervals} subintervals in all); direct LDL^T Newton (reference algorithm, oracle "
+                    f"built -march=native); {el:.1f} s",
           "newton_per_system_step": smp.newton_iterations / smp.system_steps,
           "product_library_loaded": "libpppc_b200" in maps}
     cfg = config_dict(args, prob)
