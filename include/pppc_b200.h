@@ -157,7 +157,9 @@ typedef struct {
   ps_krylov_settings pcg;   /* Jacobi-PCG for every step system (replaces SimplicialLDLT) */
   ps_krylov_settings cocg;  /* Jacobi-COCG per harmonic block (replaces complex SparseLU) */
   int32_t max_batch;        /* systems resident per batch (0 = subintervals) */
-  int32_t pad_;
+  int32_t engine;           /* fine batches of nonlinear element problems: 0 = by size (one block per
+                               system when its vectors fit in shared memory, else one warp lane per
+                               system), 1 = lane engine, 2 = block engine */
 } ps_solver_settings;
 
 /* Outcome of one batched call.  On error `code` != PS_OK and `failed_index`

@@ -65,7 +65,7 @@ class ps_krylov_settings(C.Structure):
 
 class ps_solver_settings(C.Structure):
     _fields_ = [("newton", ps_newton_settings), ("pcg", ps_krylov_settings),
-                ("cocg", ps_krylov_settings), ("max_batch", C.c_int32), ("pad_", C.c_int32)]
+                ("cocg", ps_krylov_settings), ("max_batch", C.c_int32), ("engine", C.c_int32)]
 
 
 class ps_batch_status(C.Structure):

@@ -106,7 +106,8 @@ class KrylovSettings:
 
 
 def solver_settings(newton: Optional[NewtonSettings] = None, pcg: Optional[KrylovSettings] = None,
-                    cocg: Optional[KrylovSettings] = None, max_batch: int = 0) -> _abi.ps_solver_settings:
+                    cocg: Optional[KrylovSettings] = None, max_batch: int = 0,
+                    engine: int = 0) -> _abi.ps_solver_settings:
     newton = newton or NewtonSettings()
     pcg = pcg or KrylovSettings()
     cocg = cocg or KrylovSettings()
@@ -118,6 +119,7 @@ def solver_settings(newton: Optional[NewtonSettings] = None, pcg: Optional[Krylo
     s.cocg.tol_rel, s.cocg.max_iter = cocg.tol_rel, cocg.max_iter
     s.cocg.warm_start = 1 if cocg.warm_start else 0
     s.max_batch = max_batch
+    s.engine = engine
     return s
 
 
@@ -424,7 +426,7 @@ class Propagator:
 
     def __init__(self, problem: PeriodicProblem, mesh: TimeMesh, newton: Optional[NewtonSettings] = None,
                  pcg: Optional[KrylovSettings] = None, cocg: Optional[KrylovSettings] = None,
-                 max_batch: int = 0, stream: Optional[int] = None, _ctx=None):
+                 max_batch: int = 0, stream: Optional[int] = None, _ctx=None, engine: int = 0):
         self.problem = problem
         self.mesh = mesh
         self.newton = newton or NewtonSettings()
@@ -434,7 +436,8 @@ class Propagator:
         if _ctx is not None:
             self._ctx = _ctx
             return
-        self._settings = solver_settings(self.newton, self.pcg, self.cocg, max_batch)
+        # engine: 0 by size, 1 lane engine, 2 block engine (ps_solver_settings.engine)
+        self._settings = solver_settings(self.newton, self.pcg, self.cocg, max_batch, engine)
         ctx = C.c_void_p()
         m = mesh.c()
         rc = lib().ps_create(C.byref(problem.desc), C.byref(m), C.byref(self._settings),

@@ -519,6 +519,8 @@ struct PropResult {
 // against 34.5 s per step; profiles/r02_engines.log).
 bool use_sysblock(const ps_ctx* ctx, bool linear_path, bool probe_refill) {
   if (linear_path || probe_refill || !ctx->P.sb_ok) return false;
+  if (ctx->settings.engine == 1) return false;
+  if (ctx->settings.engine == 2) return true;
   static const char* env = std::getenv("PPPC_ENGINE");
   if (env && std::strcmp(env, "lane") == 0) return false;
   if (env && std::strcmp(env, "sys") == 0) return true;
@@ -920,6 +922,8 @@ int create_ctx(const ps_problem_desc* desc, const ps_time_mesh* mesh, const ps_s
     } else {
       ps_default_settings(&ctx->settings);
     }
+    if (ctx->settings.engine < 0 || ctx->settings.engine > 2)
+      throw Failure(PS_ERR_BAD_ARG, "propagator: engine must be 0 (by size), 1 (lane) or 2 (block)");
     ctx->max_batch = ctx->settings.max_batch > 0 ? ctx->settings.max_batch : mesh->subintervals;
     if (stream) {
       ctx->stream = static_cast<cudaStream_t>(stream);

@@ -419,3 +419,34 @@ def test_pppc_cocg_warm_start_matches_oracle(name):
     # few iterations apart (radial cable, iteration 1: 161 device / 139 oracle)
     wo = hist_o["cocg_per_iteration"]
     assert abs(sum(w) - sum(wo)) <= 0.1 * sum(wo), (w, wo)
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("name", ["polar", "polar_steel_hub", "radial", "config2_geometry"])
+def test_fine_batch_both_engines_match_oracle(engine, name):
+    """The lane engine (propagate_kernel, engine 1) and the system-per-block engine
+    (sysblock_kernel, engine 2) each against the oracle: 1e-9 and the same Newton
+    totals, on the polar cable (hub row of shared values), an all-steel hub (hub
+    row of per-system values), the reference's radial cable and the configs[1]
+    geometry at reduced size."""
+    if name == "polar":
+        prob, count, s, sigma = small_polar(), 6, 4, 1e-4
+    elif name == "polar_steel_hub":
+        prob, count, s, sigma = ps.build_polar_cable(nr=10, ntheta=40, r_conductor=1e-5, r_insulator=2e-5), 5, 3, 1e-3
+    elif name == "radial":
+        prob, count, s, sigma = ps.build_coax_cable(n_r=51), 8, 5, 1e-4
+    else:
+        prob, count, s, sigma = ps.build_polar_cable(nr=20, ntheta=32), 4, 20, 1e-3
+    mesh = ps.TimeMesh(max(count, 4) * 5, s, prob.period)
+    prop = ps.Propagator(prob, mesh, NEWTON_BASELINE, max_batch=count, engine=engine)
+    U0 = np.stack([ps.seeded_normal(19051307 + n, prob.dim, sigma) for n in range(1, count + 1)])
+    F = prop.fine_propagate_batch(1, U0)
+    st = prop.last_status
+    orc = po.Oracle(prob)
+    F_o = orc.fine_propagate_batch(mesh, 1, U0, newton=NEWTON_BASELINE, mode=po.ITERATIVE)
+    for n in range(count):
+        assert rel_l2(F[n], F_o[n]) <= TOL, n
+    assert st.newton_iterations == orc.last_stats.newton_iterations
+    # the batch split does not change a system's result (bitwise)
+    F2 = np.concatenate([prop.fine_propagate_batch(1, U0[:1]), prop.fine_propagate_batch(2, U0[1:])])
+    assert np.array_equal(F, F2)
