@@ -14,6 +14,7 @@ at that size. Per N it reports:
 Start states are N(0, 1e-3), generated on the device (torch, seeded).
 
   python tools/config5_sizing.py [--N 16 64 256] [--pcg-tol 1e-6]
+  python tools/config5_sizing.py --N 16 --fine-steps 10 --newton-max 50 --pcg-tol 1e-12   (the real sweep at N = 16)
 """
 import argparse
 import ctypes as C
@@ -36,6 +37,8 @@ ap.add_argument("--pcg-tol", type=float, default=1e-2)
 ap.add_argument("--pcg-max", type=int, default=5000)
 ap.add_argument("--newton-max", type=int, default=1, help="1: one Newton iteration (stops with 'did not converge')")
 ap.add_argument("--no-probes", action="store_true")
+ap.add_argument("--fine-steps", type=int, default=1,
+                help="1: the first fine step only (mesh N*10 x 1); 10: the full configs[4] subintervals (mesh N x 10)")
 a = ap.parse_args()
 
 t0 = time.perf_counter()
@@ -53,7 +56,8 @@ for N in a.N:
     mesh = ps.TimeMesh(N, 10, prob.period)
     newton = ps.NewtonSettings(tol_abs=1e-9, tol_rel=1e-10, max_iter=a.newton_max,
                                line_search=0 if a.newton_max == 1 else 30)
-    prop = ps.Propagator(prob, ps.TimeMesh(N * 10, 1, prob.period), newton,
+    pmesh = ps.TimeMesh(N * 10, 1, prob.period) if a.fine_steps == 1 else ps.TimeMesh(N, a.fine_steps, prob.period)
+    prop = ps.Propagator(prob, pmesh, newton,
                          ps.KrylovSettings(tol_rel=a.pcg_tol, max_iter=a.pcg_max), max_batch=N)
     g = torch.Generator(device=dev)
     g.manual_seed(19051307 + N)
@@ -75,7 +79,8 @@ for N in a.N:
         probes[f"mode{mode}"] = {"us": ms.value * 1e3, "GBps": by.value / (ms.value / 1e3) / 1e9,
                                  "frac": by.value / (ms.value / 1e3) / 1e9 / peak}
     what = ("one Newton iteration of the first fine step" if a.newton_max == 1 else
-            f"the first fine step (Newton <= {a.newton_max} iterations)")
+            f"the first fine step (Newton <= {a.newton_max} iterations)" if a.fine_steps == 1 else
+            f"all {a.fine_steps} fine steps of every subinterval (Newton <= {a.newton_max} iterations per step)")
     line = {"measurement": f"BASELINE configs[4]: {what}, PCG rel {a.pcg_tol}",
             "nr": a.nr, "ntheta": a.ntheta, "dof": d, "nnz": prob.nnz, "N": N, "build_s": build_s,
             "device_used_GB": (total - free) / 1e9, "device_total_GB": total / 1e9,
@@ -85,7 +90,9 @@ for N in a.N:
             "frac": st.algorithmic_bytes / (st.kernel_ms / 1e3) / 1e9 / peak, "phase_probes": probes,
             "status": st.code, "max_pcg_per_solve": st.max_pcg_iterations,
             "max_newton": st.max_newton_iterations, "newton_max": a.newton_max,
-            "dof_timesteps_per_s": (N * d / (st.kernel_ms / 1e3)) if a.newton_max > 1 and st.code == 0 else None,
+            "fine_steps": a.fine_steps,
+            "dof_timesteps_per_s": (N * a.fine_steps * d / (st.kernel_ms / 1e3)) if a.newton_max > 1 and st.code == 0
+            else None,
             "failed_residual": st.residual if st.code else None}
     print(json.dumps(line), flush=True)
     prop.close()

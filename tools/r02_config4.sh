@@ -1,10 +1,11 @@
 #!/bin/bash
-# BASELINE configs[4] on one B200 (bounded): the first fine step of N = 16 with the real
-# Newton / PCG 1e-12, then one Newton iteration (step solve to PCG 1e-12) at N = 64 and 256.
-mkdir -p gpurun_out
-case "$1" in
-  a) timeout 3300 python tools/config5_sizing.py --N 16 --newton-max 50 --pcg-tol 1e-12 --pcg-max 50000 --no-probes \
-       > gpurun_out/c4_n16.jsonl 2> gpurun_out/c4_n16.err; echo rc=$?; tail -2 gpurun_out/c4_n16.err ;;
-  b) timeout 3300 python tools/config5_sizing.py --N 256 64 --newton-max 1 --pcg-tol 1e-12 --pcg-max 50000 \
-       > gpurun_out/c4_n256_64.jsonl 2> gpurun_out/c4_n256_64.err; echo rc=$?; tail -2 gpurun_out/c4_n256_64.err ;;
-esac
+# BASELINE configs[4] on one B200 (k2 = 4.0, I0 = 8000 A, d = 4,093,953):
+#  a) N = 16: all 10 fine steps of every subinterval, Newton (max 50, backtracking) to
+#     1e-10 rel / 1e-9 abs, PCG 1e-12 -> DOF-timesteps/s, HBM in use, Newton/PCG counts
+#  b) N = 64 and 256: one Newton iteration of the first fine step at PCG 1e-12 (memory fit
+#     and throughput at scale; the full 10 steps at N = 256 would take hours)
+O=gpurun_out/config4; mkdir -p $O
+timeout 3000 python tools/config5_sizing.py --N 16 --fine-steps 10 --newton-max 50 --pcg-tol 1e-12 --pcg-max 50000 \
+   --no-probes > $O/c4_n16_10steps.jsonl 2> $O/c4_n16_10steps.err; echo a_rc=$?; tail -c 1500 $O/c4_n16_10steps.jsonl; tail -2 $O/c4_n16_10steps.err
+timeout 1500 python tools/config5_sizing.py --N 64 256 --newton-max 1 --pcg-tol 1e-12 --pcg-max 50000 \
+   > $O/c4_n64_256.jsonl 2> $O/c4_n64_256.err; echo b_rc=$?; tail -c 2500 $O/c4_n64_256.jsonl; tail -2 $O/c4_n64_256.err
