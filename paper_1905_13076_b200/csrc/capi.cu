@@ -129,6 +129,10 @@ struct ps_ctx {
   double *sb_u = nullptr, *sb_A = nullptr, *sb_hub = nullptr;
   size_t sb_u_len = 0, sb_A_len = 0, sb_hub_len = 0;
   std::map<double, StepMatrix> step_cache;
+  // system-per-cluster engine geometry (cluster_geometry): C = 0 when it cannot run
+  ClusterGeom cl_geo{};
+  int cl_slots = 0;       // co-resident clusters
+  bool cl_sized = false;
   SpectralState* spec = nullptr;
   int spec_N = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -507,24 +511,91 @@ struct PropResult {
   double* state = nullptr;  // interleaved result (stride = count)
 };
 
-// Fine-propagation engine for a nonlinear element problem: the system-per-block
-// kernel (one block per system, block barriers only) or the lane kernel (one
-// warp lane per system, groups of blocks with device-wide group barriers).
-// PPPC_ENGINE=sys|lane forces one.  By default the system-per-block kernel runs
-// when the pattern qualifies (DevProblem::sb_ok) and a system's seven vectors
-// fit in one block's shared memory: small systems are latency-bound and gain
-// most from block barriers (configs[0], d = 2,497: fine sweep 9.8 -> 5.2 s per
-// 35 PP-PC iterations); at configs[1] size (d = 50,945) the lane kernel, which
-// reads the pattern and shared values once for 32 systems, is faster (25.8 s
-// against 34.5 s per step; profiles/r02_engines.log).
-bool use_sysblock(const ps_ctx* ctx, bool linear_path, bool probe_refill) {
-  if (linear_path || probe_refill || !ctx->P.sb_ok) return false;
-  if (ctx->settings.engine == 1) return false;
-  if (ctx->settings.engine == 2) return true;
+// Row split and column windows of the system-per-cluster engine for C CTAs:
+// balanced contiguous row ranges; a CTA's window spans its rows and every
+// column they gather (the hub row excluded: its product goes through the sum).
+ClusterGeom cluster_split(const DevProblem& P, int C) {
+  ClusterGeom g{};
+  g.C = C;
+  for (int c = 0; c <= C; ++c) g.row_begin[c] = static_cast<int>(static_cast<int64_t>(P.d) * c / C);
+  for (int c = 0; c < C; ++c) {
+    const int r0 = g.row_begin[c], r1 = g.row_begin[c + 1];
+    int lo = r0, hi = r1;
+    for (int i = r0; i < r1; ++i) {
+      if (i == P.sb_hub) continue;
+      for (int k = P.h_rp[i]; k < P.h_rp[i + 1]; ++k) {
+        lo = std::min(lo, P.h_ci[k]);
+        hi = std::max(hi, P.h_ci[k] + 1);
+      }
+    }
+    g.win_lo[c] = lo;
+    g.win_hi[c] = hi;
+    g.rows_max = std::max(g.rows_max, r1 - r0);
+    g.win_max = std::max(g.win_max, hi - lo);
+  }
+  return g;
+}
+
+// Picks the cluster size: every C whose CTA working set (p window, r, x) fits in
+// shared memory and whose row range fits the per-thread register rows; among
+// them the one that keeps most SMs busy (C x co-resident clusters), the smaller
+// C on ties.  PPPC_CLUSTER=C forces a size.
+void cluster_geometry(ps_ctx* ctx) {
+  if (ctx->cl_sized) return;
+  ctx->cl_sized = true;
+  const DevProblem& P = ctx->P;
+  if (!P.sb_ok) return;
+  int dev = 0, smem_max = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int forced = std::getenv("PPPC_CLUSTER") ? std::atoi(std::getenv("PPPC_CLUSTER")) : 0;
+  int best_cover = 0;
+  for (int C = 1; C <= kClusterMaxC; ++C) {
+    if (forced > 0 && C != forced) continue;
+    if (C > P.d) break;
+    const ClusterGeom g = cluster_split(P, C);
+    if (g.rows_max > syscluster_max_rows() || syscluster_smem(g) > static_cast<size_t>(smem_max)) continue;
+    const int slots = syscluster_max_clusters(P.npe, g);
+    if (slots < 1) continue;
+    if (slots * C > best_cover) {
+      best_cover = slots * C;
+      ctx->cl_geo = g;
+      ctx->cl_slots = slots;
+    }
+  }
+  if (std::getenv("PPPC_DEBUG_TIMING") && ctx->cl_geo.C > 0)
+    std::fprintf(stderr, "[pppc cluster] C = %d, rows/CTA %d, window %d, smem %zu B, %d co-resident clusters\n",
+                 ctx->cl_geo.C, ctx->cl_geo.rows_max, ctx->cl_geo.win_max, syscluster_smem(ctx->cl_geo),
+                 ctx->cl_slots);
+}
+
+// Fine-propagation engine for a nonlinear element problem.
+//   block   (sysblock_kernel): one block per system, block barriers only; best
+//           when a system's seven vectors fit in one block's shared memory
+//           (configs[0], d = 2,497: fine sweep 9.8 -> 5.2 s per 35 PP-PC iterations);
+//   cluster (syscluster_kernel): one thread-block cluster per system, Krylov
+//           vectors in the cluster's shared memory / registers, hardware cluster
+//           barriers; for systems too large for one block whose vectors fit in a
+//           cluster (configs[1], d = 50,945);
+//   lane    (propagate_kernel): one warp lane per system, groups of blocks with
+//           device-wide group barriers, vectors in HBM; any size (configs[3]/[4]).
+// ps_solver_settings.engine (1 lane, 2 block, 3 cluster) or PPPC_ENGINE=lane|sys|cluster
+// forces one; the pattern must qualify (DevProblem::sb_ok) for block and cluster.
+enum class Engine { Lane, Block, Cluster };
+Engine select_engine(ps_ctx* ctx, bool linear_path, bool probe_refill) {
+  if (linear_path || probe_refill || !ctx->P.sb_ok) return Engine::Lane;
+  const int e = ctx->settings.engine;
+  if (e == 1) return Engine::Lane;
+  if (e == 2) return Engine::Block;
   static const char* env = std::getenv("PPPC_ENGINE");
-  if (env && std::strcmp(env, "lane") == 0) return false;
-  if (env && std::strcmp(env, "sys") == 0) return true;
-  return sysblock_smem(ctx->P.d) <= kSbSmemMax;
+  if (e == 0 && env && std::strcmp(env, "lane") == 0) return Engine::Lane;
+  if (e == 0 && env && std::strcmp(env, "sys") == 0) return Engine::Block;
+  const bool want_cluster = e == 3 || (env && std::strcmp(env, "cluster") == 0);
+  if (!want_cluster && sysblock_smem(ctx->P.d) <= kSbSmemMax) return Engine::Block;
+  cluster_geometry(ctx);
+  if (ctx->cl_geo.C > 0) return Engine::Cluster;
+  if (e == 3) throw Failure(PS_ERR_BAD_ARG, "propagator: the cluster engine cannot hold this system on chip");
+  return Engine::Lane;
 }
 
 // Runs `steps` implicit-Euler steps of size dt for `count` systems whose
@@ -664,7 +735,8 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   static const bool debug_timing = std::getenv("PPPC_DEBUG_TIMING") != nullptr;
   unsigned long long* dbg = nullptr;
   const int nblk = geo.G * geo.C;
-  const bool sysblock = use_sysblock(ctx, linear_path, probe_refill);
+  const Engine engine = select_engine(ctx, linear_path, probe_refill);
+  const bool sysblock = engine != Engine::Lane;
   if (debug_timing && !sysblock && dalloc(&dbg, static_cast<size_t>(nblk) * kDbgSlots)) K.dbg = dbg;
   // The SpMV gathers the search direction p at +-ntheta rows; keep p resident in
   // L2 (persisting access-policy window) so the streamed matrix values and
@@ -708,10 +780,11 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
     sp.KT = P.KT;
     sp.AshT = shared_step_matrix(ctx, dt).AT;
     static const bool no_smem = std::getenv("PPPC_SB_NO_SMEM") != nullptr;
-    sp.smem_vectors = (!no_smem && sysblock_smem(P.d) <= kSbSmemMax) ? 1 : 0;
+    sp.smem_vectors = (engine == Engine::Block && !no_smem && sysblock_smem(P.d) <= kSbSmemMax) ? 1 : 0;
     check(cudaMemsetAsync(ctx->lockstep, 0, geo.G * sizeof(int64_t), ctx->stream), "lockstep reset");
     check(cudaEventRecord(ctx->e0, ctx->stream), "event");
-    const int rc = launch_sysblock(K, sp, npe, ctx->stream, &err);
+    const int rc = engine == Engine::Cluster ? launch_syscluster(K, sp, ctx->cl_geo, npe, ctx->stream, &err)
+                                             : launch_sysblock(K, sp, npe, ctx->stream, &err);
     if (rc != PS_OK) throw Failure(rc, err);
   } else if (sequential_groups() && geo.G > 1) {
     // one launch per group, each on all C blocks, own arrival counter
@@ -922,8 +995,8 @@ int create_ctx(const ps_problem_desc* desc, const ps_time_mesh* mesh, const ps_s
     } else {
       ps_default_settings(&ctx->settings);
     }
-    if (ctx->settings.engine < 0 || ctx->settings.engine > 2)
-      throw Failure(PS_ERR_BAD_ARG, "propagator: engine must be 0 (by size), 1 (lane) or 2 (block)");
+    if (ctx->settings.engine < 0 || ctx->settings.engine > 3)
+      throw Failure(PS_ERR_BAD_ARG, "propagator: engine must be 0 (by size), 1 (lane), 2 (block) or 3 (cluster)");
     ctx->max_batch = ctx->settings.max_batch > 0 ? ctx->settings.max_batch : mesh->subintervals;
     if (stream) {
       ctx->stream = static_cast<cudaStream_t>(stream);

@@ -21,6 +21,8 @@
 #include "group_sync.cuh"
 #include "pppc_internal.h"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <type_traits>
 #include <cstdio>
@@ -1616,6 +1618,8 @@ __global__ void __launch_bounds__(NT, 1) sysblock_kernel(const PropParams P, con
   }
 }
 
+#include "cluster_engine.cuh"
+
 // ------------------------------------------------------- phase probes
 // One PCG phase over the whole batch with the propagation kernel's exact thread
 // -> (group, row, lane) mapping and code, but no barriers or state machine:
@@ -1912,6 +1916,76 @@ int launch_sysblock(const PropParams& prm, const SysParams& sp, int npe, cudaStr
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     if (err) *err = std::string("cuda: sysblock launch failed: ") + cudaGetErrorString(e);
+    return PS_ERR_CUDA;
+  }
+  return PS_OK;
+}
+
+static_assert(kClMaxC == kClusterMaxC, "cluster geometry arrays");
+
+size_t syscluster_smem(const ClusterGeom& gm) {
+  return (static_cast<size_t>(gm.win_max) + 2 * static_cast<size_t>(gm.rows_max)) * sizeof(double) + sizeof(ClShared);
+}
+
+int syscluster_max_rows() { return kClRpt * kClThreads; }
+
+namespace {
+void* syscluster_fn(int npe) {
+  return npe == 2 ? reinterpret_cast<void*>(&syscluster_kernel<2>) : reinterpret_cast<void*>(&syscluster_kernel<3>);
+}
+
+bool syscluster_config(int npe, const ClusterGeom& gm, int count, cudaStream_t st, cudaLaunchConfig_t* cfg,
+                       cudaLaunchAttribute* attr) {
+  void* fn = syscluster_fn(npe);
+  const size_t smem = syscluster_smem(gm);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+    return false;
+  if (gm.C > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return false;
+  *cfg = cudaLaunchConfig_t{};
+  cfg->gridDim = dim3(static_cast<unsigned>(count) * gm.C);
+  cfg->blockDim = dim3(kClThreads);
+  cfg->dynamicSmemBytes = smem;
+  cfg->stream = st;
+  attr->id = cudaLaunchAttributeClusterDimension;
+  attr->val.clusterDim.x = gm.C;
+  attr->val.clusterDim.y = 1;
+  attr->val.clusterDim.z = 1;
+  cfg->attrs = attr;
+  cfg->numAttrs = 1;
+  return true;
+}
+}  // namespace
+
+int syscluster_max_clusters(int npe, const ClusterGeom& gm) {
+  if (npe != 2 && npe != 3) return 0;
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute attr;
+  if (!syscluster_config(npe, gm, 1, nullptr, &cfg, &attr)) {
+    cudaGetLastError();
+    return 0;
+  }
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, syscluster_fn(npe), &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int launch_syscluster(const PropParams& prm, const SysParams& sp, const ClusterGeom& gm, int npe, cudaStream_t st,
+                      std::string* err) {
+  if (npe != 2 && npe != 3) return PS_ERR_BAD_ARG;
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute attr;
+  if (!syscluster_config(npe, gm, prm.count, st, &cfg, &attr)) {
+    if (err) *err = std::string("cuda: cluster engine setup failed: ") + cudaGetErrorString(cudaGetLastError());
+    return PS_ERR_CUDA;
+  }
+  const cudaError_t e = npe == 2 ? cudaLaunchKernelEx(&cfg, syscluster_kernel<2>, prm, sp, gm)
+                                 : cudaLaunchKernelEx(&cfg, syscluster_kernel<3>, prm, sp, gm);
+  if (e != cudaSuccess) {
+    if (err) *err = std::string("cuda: cluster engine launch failed: ") + cudaGetErrorString(e);
     return PS_ERR_CUDA;
   }
   return PS_OK;

@@ -140,6 +140,20 @@ struct SysParams {
 size_t sysblock_smem(int d);
 constexpr size_t kSbSmemMax = 200 * 1024;
 
+// System-per-cluster engine (cluster_engine.cuh): a thread-block cluster of C
+// CTAs runs one system; CTA c owns the contiguous rows [row_begin[c],
+// row_begin[c+1]) and keeps p over the column window [win_lo[c], win_hi[c])
+// (its rows plus the halo they gather), r and x of its rows in shared memory.
+constexpr int kClusterMaxC = 16;
+struct ClusterGeom {
+  int C;
+  int rows_max;   // largest row range
+  int win_max;    // largest window
+  int row_begin[kClusterMaxC + 1];
+  int win_lo[kClusterMaxC];
+  int win_hi[kClusterMaxC];
+};
+
 // Device-resident problem + work buffers owned by a context.
 struct DevProblem {
   int d = 0, nnz = 0;
@@ -209,6 +223,13 @@ void launch_eval_curve(const ps_curve& c, int n, const double* b2, double* nu, d
 void launch_frozen_K(const DevProblem& p, const double* u_ref, double* K_out, cudaStream_t st);
 int launch_phase_probe(const PropParams& prm, int mode, double* sink, cudaStream_t st);
 int launch_sysblock(const PropParams& prm, const SysParams& sp, int npe, cudaStream_t st, std::string* err);
+// system-per-cluster engine: shared memory of one CTA, rows a CTA can own at most,
+// co-resident clusters (0 = this geometry cannot launch), launch
+size_t syscluster_smem(const ClusterGeom& gm);
+int syscluster_max_rows();
+int syscluster_max_clusters(int npe, const ClusterGeom& gm);
+int launch_syscluster(const PropParams& prm, const SysParams& sp, const ClusterGeom& gm, int npe, cudaStream_t st,
+                      std::string* err);
 
 // spectral (spectral.cu)
 struct SpectralState;

@@ -421,14 +421,18 @@ def test_pppc_cocg_warm_start_matches_oracle(name):
     assert abs(sum(w) - sum(wo)) <= 0.1 * sum(wo), (w, wo)
 
 
-@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("engine", [1, 2, 3, (3, 2), (3, 3), (3, 5), (3, 8)])
 @pytest.mark.parametrize("name", ["polar", "polar_steel_hub", "radial", "config2_geometry"])
-def test_fine_batch_both_engines_match_oracle(engine, name):
-    """The lane engine (propagate_kernel, engine 1) and the system-per-block engine
-    (sysblock_kernel, engine 2) each against the oracle: 1e-9 and the same Newton
-    totals, on the polar cable (hub row of shared values), an all-steel hub (hub
-    row of per-system values), the reference's radial cable and the configs[1]
-    geometry at reduced size."""
+def test_fine_batch_both_engines_match_oracle(engine, name, monkeypatch):
+    """The lane engine (propagate_kernel, engine 1), the system-per-block engine
+    (sysblock_kernel, engine 2) and the system-per-cluster engine (syscluster_kernel,
+    engine 3; also with the cluster size forced to 2, 3, 5 and 8 CTAs) each against
+    the oracle: 1e-9 and the same Newton totals, on the polar cable (hub row of
+    shared values), an all-steel hub (hub row of per-system values), the reference's
+    radial cable and the configs[1] geometry at reduced size."""
+    if isinstance(engine, tuple):
+        monkeypatch.setenv("PPPC_CLUSTER", str(engine[1]))
+        engine = engine[0]
     if name == "polar":
         prob, count, s, sigma = small_polar(), 6, 4, 1e-4
     elif name == "polar_steel_hub":
