@@ -513,7 +513,7 @@ struct PropResult {
 
 // Row split and column windows of the system-per-cluster engine for C CTAs:
 // balanced contiguous row ranges; a CTA's window spans its rows and every
-// column they gather (the hub row excluded: its product goes through the sum).
+// column they gather (the hub row included: its owner forms the whole product).
 ClusterGeom cluster_split(const DevProblem& P, int C) {
   ClusterGeom g{};
   g.C = C;
@@ -522,7 +522,6 @@ ClusterGeom cluster_split(const DevProblem& P, int C) {
     const int r0 = g.row_begin[c], r1 = g.row_begin[c + 1];
     int lo = r0, hi = r1;
     for (int i = r0; i < r1; ++i) {
-      if (i == P.sb_hub) continue;
       for (int k = P.h_rp[i]; k < P.h_rp[i + 1]; ++k) {
         lo = std::min(lo, P.h_ci[k]);
         hi = std::max(hi, P.h_ci[k] + 1);
@@ -536,8 +535,8 @@ ClusterGeom cluster_split(const DevProblem& P, int C) {
   return g;
 }
 
-// Picks the cluster size: every C whose CTA working set (p window, r, x) fits in
-// shared memory and whose row range fits the per-thread register rows; among
+// Picks the cluster size: every C whose CTA working set (p window, r, x, q) fits in
+// shared memory and whose row range fits the per-thread row masks; among
 // them the one that keeps most SMs busy (C x co-resident clusters), the smaller
 // C on ties.  PPPC_CLUSTER=C forces a size.
 void cluster_geometry(ps_ctx* ctx) {

@@ -1924,10 +1924,10 @@ int launch_sysblock(const PropParams& prm, const SysParams& sp, int npe, cudaStr
 static_assert(kClMaxC == kClusterMaxC, "cluster geometry arrays");
 
 size_t syscluster_smem(const ClusterGeom& gm) {
-  return (static_cast<size_t>(gm.win_max) + 2 * static_cast<size_t>(gm.rows_max)) * sizeof(double) + sizeof(ClShared);
+  return (static_cast<size_t>(gm.win_max) + 3 * static_cast<size_t>(gm.rows_max)) * sizeof(double) + sizeof(ClShared);
 }
 
-int syscluster_max_rows() { return kClRpt * kClThreads; }
+int syscluster_max_rows() { return kClMaxRpt * kClThreads; }
 
 namespace {
 void* syscluster_fn(int npe) {
