@@ -371,6 +371,55 @@ void build_problem(ps_ctx* ctx, const ps_problem_desc* desc) {
       P.KT = upload(kT.data(), kT.size(), "padded stiffness columns");
       P.sb_ok = true;
       P.sb_hub = hub;
+      for (int i = 0; i < P.d; ++i) {
+        const int len = P.h_rp[i + 1] - P.h_rp[i];
+        if (len <= kEll) P.ell_width = std::max(P.ell_width, len);
+      }
+      // Sparsity-pattern dictionary for the cluster engine: a row's pattern is its
+      // length and its columns relative to the row (the hub's column, which every
+      // neighbour of the hub holds, is kept absolute).  Structured meshes have a
+      // handful of patterns; the kPatMax - 1 most frequent get an id, the other
+      // rows stay "irregular" and read their padded columns from memory.
+      std::map<std::vector<int>, int> freq;
+      auto key_of = [&](int i) {
+        const int b = P.h_rp[i], len = P.h_rp[i + 1] - b;
+        std::vector<int> key(2 + kEll, 0);
+        int absmask = 0;
+        for (int k = 0; k < len; ++k) {
+          const int c = P.h_ci[b + k];
+          if (c == hub && c != i) {
+            absmask |= 1 << k;
+            key[2 + k] = c;
+          } else {
+            key[2 + k] = c - i;
+          }
+        }
+        key[0] = len;
+        key[1] = absmask;
+        return key;
+      };
+      for (int i = 0; i < P.d; ++i)
+        if (P.h_rp[i + 1] - P.h_rp[i] <= kEll) ++freq[key_of(i)];
+      std::vector<std::pair<int, std::vector<int>>> order;
+      for (const auto& kv : freq) order.emplace_back(kv.second, kv.first);
+      std::stable_sort(order.begin(), order.end(),
+                       [](const auto& a, const auto& b) { return a.first > b.first; });
+      std::map<std::vector<int>, int> ids;
+      std::vector<int> pcols(static_cast<size_t>(kPatMax) * kEll, 0), pmeta(kPatMax, 0);
+      for (size_t n = 0; n < order.size() && n < static_cast<size_t>(kPatIrregular); ++n) {
+        ids[order[n].second] = static_cast<int>(n);
+        for (int k = 0; k < kEll; ++k) pcols[n * kEll + k] = order[n].second[2 + k];
+        pmeta[n] = order[n].second[0] | (order[n].second[1] << 8);
+      }
+      std::vector<unsigned char> pid(P.d, static_cast<unsigned char>(kPatIrregular));
+      for (int i = 0; i < P.d; ++i) {
+        if (P.h_rp[i + 1] - P.h_rp[i] > kEll) continue;
+        const auto it = ids.find(key_of(i));
+        if (it != ids.end()) pid[i] = static_cast<unsigned char>(it->second);
+      }
+      P.pat_id = upload(pid.data(), pid.size(), "pattern ids");
+      P.pat_cols = upload(pcols.data(), pcols.size(), "pattern columns");
+      P.pat_meta = upload(pmeta.data(), pmeta.size(), "pattern lengths");
     }
   }
   P.nterms = desc->n_terms;
@@ -554,7 +603,7 @@ void cluster_geometry(ps_ctx* ctx) {
     if (C > P.d) break;
     const ClusterGeom g = cluster_split(P, C);
     if (g.rows_max > syscluster_max_rows() || syscluster_smem(g) > static_cast<size_t>(smem_max)) continue;
-    const int slots = syscluster_max_clusters(P.npe, g);
+    const int slots = syscluster_max_clusters(P.npe, P.ell_width, g);
     if (slots < 1) continue;
     if (slots * C > best_cover) {
       best_cover = slots * C;
@@ -737,6 +786,12 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   const Engine engine = select_engine(ctx, linear_path, probe_refill);
   const bool sysblock = engine != Engine::Lane;
   if (debug_timing && !sysblock && dalloc(&dbg, static_cast<size_t>(nblk) * kDbgSlots)) K.dbg = dbg;
+  unsigned long long* cl_dbg = nullptr;
+  if (debug_timing && engine == Engine::Cluster &&
+      dalloc(&cl_dbg, static_cast<size_t>(count) * ctx->cl_geo.C * 8)) {
+    cudaMemsetAsync(cl_dbg, 0, static_cast<size_t>(count) * ctx->cl_geo.C * 8 * sizeof(unsigned long long), ctx->stream);
+    K.dbg = cl_dbg;
+  }
   // The SpMV gathers the search direction p at +-ntheta rows; keep p resident in
   // L2 (persisting access-policy window) so the streamed matrix values and
   // vectors do not evict it between neighbour reads.  PPPC_NO_L2_PERSIST=1 off.
@@ -775,6 +830,10 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
       sp.hubA = ctx->sb_hub;
     }
     sp.ciT = P.ciT;
+    sp.pat_id = P.pat_id;
+    sp.pat_cols = P.pat_cols;
+    sp.pat_meta = P.pat_meta;
+    sp.ell_width = P.ell_width;
     sp.MT = P.MT;
     sp.KT = P.KT;
     sp.AshT = shared_step_matrix(ctx, dt).AT;
@@ -801,6 +860,24 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
     if (rc != PS_OK) throw Failure(rc, err);
   }
   check(cudaEventRecord(ctx->e1, ctx->stream), "event");
+  if (cl_dbg) {
+    // cluster engine: mean cycles per PCG iteration of the four parts, over all CTAs
+    std::vector<unsigned long long> h(static_cast<size_t>(count) * ctx->cl_geo.C * 8);
+    check(cudaMemcpyAsync(h.data(), cl_dbg, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream), "dbg");
+    check(cudaStreamSynchronize(ctx->stream), "dbg");
+    cudaFree(cl_dbg);
+    K.dbg = nullptr;
+    double tm[4] = {0, 0, 0, 0}, its = 0;
+    for (size_t b = 0; b < h.size() / 8; ++b) {
+      for (int k = 0; k < 4; ++k) tm[k] += static_cast<double>(h[b * 8 + k]);
+      its += static_cast<double>(h[b * 8 + 4]);
+    }
+    if (its > 0)
+      std::fprintf(stderr,
+                   "[pppc cluster timing] cycles per PCG iteration: SpMV pass %.0f, cluster sum %.0f, update pass %.0f, "
+                   "halo wait %.0f\n",
+                   tm[0] / its, tm[1] / its, tm[2] / its, tm[3] / its);
+  }
   std::vector<unsigned long long> h_dbg;
   if (K.dbg) {
     constexpr int W = kDbgSlots;
@@ -1087,7 +1164,7 @@ void ps_destroy(ps_ctx* ctx) {
     cudaFree(kv.second.AE);
     if (kv.second.AT) cudaFree(kv.second.AT);
   }
-  void* sb[] = {P.ciT, P.MT, P.KT, ctx->sb_u, ctx->sb_A, ctx->sb_hub};
+  void* sb[] = {P.ciT, P.MT, P.KT, ctx->sb_u, ctx->sb_A, ctx->sb_hub, P.pat_id, P.pat_cols, P.pat_meta};
   for (void* q : sb)
     if (q) cudaFree(q);
   if (ctx->spec) spectral_free(ctx->spec);

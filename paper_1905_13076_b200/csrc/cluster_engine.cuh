@@ -7,8 +7,10 @@
 // the Krylov vectors of a system of d ~ 50k rows stay ON CHIP for the whole
 // launch:
 //   * the search direction p of the CTA's rows plus the halo its rows gather
-//     (the window [win_lo, win_hi) of columns), the residual r, the update x and
-//     q = A p of the CTA's rows live in shared memory;
+//     (the window [win_lo, win_hi) of columns), the residual r, q = A p and the
+//     Jacobi entries of the CTA's rows live in shared memory (rows are dealt
+//     thread-cyclically, at most kClRpt per thread); the solution update x, which
+//     only the update pass touches, stays in L2;
 //   * after every update the owning thread pushes the entries of p that other
 //     CTAs' windows hold straight into their shared memory with st.async
 //     (DSMEM store + complete_tx on the receiver's mbarrier): the receiver waits
@@ -22,8 +24,13 @@
 //     and the Jacobi entry anyway), so an iteration is
 //         SpMV pass -> cluster sum of {p.q, q.z, q.Dq, r.z, r.r} -> update pass
 //     and convergence is seen one SpMV pass late (one wasted pass per solve).
-// Per PCG iteration only the matrix streams from L2 (padded columns, shared or
-// per-system slot values, Jacobi); nothing device-wide is synchronised and the
+//   * the sparsity pattern is held on chip as a dictionary: a row carries an
+//     8-bit pattern id (packed in registers), the pattern's relative columns sit
+//     in shared memory, so no column index is read from memory in the PCG loop
+//     (rows whose pattern is not among the 255 most frequent ones fall back to
+//     the padded column lists).
+// Per PCG iteration only the slot values stream from L2 (shared M/dt + K_const or
+// the system's own, row length many); nothing device-wide is synchronised and the
 // hardware schedules the clusters (one per system) as CTAs drain.  Hardware
 // cluster barriers (with their device-scope fence) are used only where global
 // memory written by one CTA is read by another (the Newton state u).
@@ -33,22 +40,30 @@
 namespace cg = cooperative_groups;
 
 #ifndef PPPC_CL_THREADS
-#define PPPC_CL_THREADS 1024
+#define PPPC_CL_THREADS 512
 #endif
 #ifndef PPPC_CL_RB
 #define PPPC_CL_RB 1
 #endif
+#ifndef PPPC_CL_RPT
+#define PPPC_CL_RPT (6656 / PPPC_CL_THREADS)
+#endif
 constexpr int kClThreads = PPPC_CL_THREADS;
-constexpr int kClRb = PPPC_CL_RB;   // rows per thread whose operands are in flight together (SpMV pass)
-constexpr int kClMaxC = 16;         // CTAs per cluster at most (8 portable)
-constexpr int kClNd = 8;            // reduction slots per CTA
-constexpr int kClMaxRpt = 32;       // rows per thread at most (row-kind / push bit masks)
+constexpr int kClRb = PPPC_CL_RB;     // rows per thread whose slot values are in flight together (SpMV pass)
+constexpr int kClRpt = PPPC_CL_RPT;   // rows per thread at most (their x entries are registers)
+constexpr int kClMaxC = 16;           // CTAs per cluster at most (8 portable)
+constexpr int kClNd = 8;              // reduction slots per CTA
+constexpr unsigned kClOwn = 0x100u, kClPush = 0x200u;
 
-struct ClShared {
+struct alignas(16) ClShared {
+  int4 pat_cols[kPatMax][kEll / 4];       // pattern dictionary: column entries
+  int pat_meta[kPatMax];                  // length | absolute mask << 8
   double red[kClNd][32];
   double cpart[2][kClMaxC][kClNd];
   double tot[kClNd];
   double qh;                              // the hub row's product (owner CTA)
+  long long tm[4], tm_c[4];               // PPPC_DEBUG_TIMING: cycles of the SpMV pass, cluster sum, update
+                                          // pass, halo wait; stamps (start, after sum, after update, mid-sum)
   unsigned long long red_mb[2], halo_mb;  // mbarriers
   int n_push;
   int push_lo[kClMaxC], push_hi[kClMaxC];
@@ -66,9 +81,11 @@ struct ClCtx {
   const double *hubD;   // Jacobi entry of the hub row (owner)
   double* pw;   // p window (index = column - wlo)
   double* rs;   // r of own rows (index = row - r0)
-  double* xs;   // x of own rows
+  double* ds;   // Jacobi entries of own rows
   double* qs;   // q of own rows
+  unsigned short* info;   // per own row: pattern id | kClOwn (per-system values) | kClPush (held by other windows)
   ClShared* sh;
+  bool timed;          // PPPC_DEBUG_TIMING: thread 0 keeps cycle stamps in shared memory
 };
 
 __device__ __forceinline__ unsigned cl_smem_u32(const void* p) {
@@ -126,61 +143,82 @@ __device__ __forceinline__ void cl_halo_sync(ClCtx& X) {
   }
 }
 
+// Sum of 8 slots over the 32 lanes in 4 + 2 + 1 + 1 + 1 exchanges (instead of
+// 8 x 5): after every exchange a lane is responsible for half as many slots.  On
+// return the lane holds the warp total of slot cl_slot_of(lane); the additions
+// form one fixed tree.
+__device__ __forceinline__ double cl_butterfly8(const double (&v)[8], int lane) {
+  double w4[4], w2[2];
+  const bool b4 = lane & 16;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double send = b4 ? v[j] : v[j + 4], keep = b4 ? v[j + 4] : v[j];
+    w4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  const bool b3 = lane & 8;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double send = b3 ? w4[j] : w4[j + 2], keep = b3 ? w4[j + 2] : w4[j];
+    w2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const bool b2 = lane & 4;
+  const double send = b2 ? w2[0] : w2[1], keep = b2 ? w2[1] : w2[0];
+  double w = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  w += __shfl_xor_sync(0xffffffffu, w, 2);
+  w += __shfl_xor_sync(0xffffffffu, w, 1);
+  return w;
+}
+__device__ __forceinline__ int cl_slot_of(int lane) { return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1); }
+__device__ __forceinline__ int cl_lane_of(int slot) { return (slot & 4 ? 16 : 0) + (slot & 2 ? 8 : 0) + (slot & 1 ? 4 : 0); }
+
 // Fixed-order cluster sum of ND values; every thread of every CTA returns the
-// same totals.  HUBFIX (PCG pass, values {p.q, q.z, q.Dq, r.z, r.r, hub part}):
-// the hub row's product is the owner's block sum of slot 5; the owner adds the
-// row's terms to its block sums before they are sent and keeps the product.
+// same totals.  HUBFIX (PCG pass, values {p.q, q.z, q.Dq, r.z, r.r}): the hub
+// row's product (sh->qh, formed by the owner's last warp during the SpMV pass)
+// enters the owner's block sums before they are sent.
 template <int ND, bool HUBFIX>
 __device__ __forceinline__ void cl_reduce(ClCtx& X, double (&v)[ND]) {
   constexpr int NW = kClThreads / 32;
   static_assert(NW <= 32 && ND <= kClNd, "reduction geometry");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   ClShared* sh = X.sh;
+  {
+    double v8[8];
 #pragma unroll
-  for (int k = 0; k < ND; ++k) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], off);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < ND; ++k) sh->red[k][warp] = v[k];
+    for (int k = 0; k < 8; ++k) v8[k] = k < ND ? v[k] : 0.0;
+    const double w = cl_butterfly8(v8, lane);
+    if ((lane & 3) == 0) sh->red[cl_slot_of(lane)][warp] = w;
   }
   __syncthreads();
+  if (X.timed && threadIdx.x == 0) sh->tm_c[3] = clock64();
   if (warp == 0) {
     unsigned long long* mb = &sh->red_mb[X.par];
-    constexpr int NS = HUBFIX ? ND - 1 : ND;   // values that cross the cluster
-    if (lane == 0) cl_mbar_expect(mb, static_cast<unsigned>(X.C) * NS * 8u);
+    if (lane == 0) cl_mbar_expect(mb, static_cast<unsigned>(X.C) * ND * 8u);
+    double v8[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v8[k] = (k < ND && lane < NW) ? sh->red[k][lane] : 0.0;
+    const double w = cl_butterfly8(v8, lane);
     double s[ND];
 #pragma unroll
-    for (int k = 0; k < ND; ++k) {
-      double w = lane < NW ? sh->red[k][lane] : 0.0;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) w += __shfl_down_sync(0xffffffffu, w, off);
-      s[k] = __shfl_sync(0xffffffffu, w, 0);
-    }
+    for (int k = 0; k < ND; ++k) s[k] = __shfl_sync(0xffffffffu, w, cl_lane_of(k));
     if (HUBFIX && X.hub >= 0) {
-      const double qh = s[ND - 1];
+      const double qh = sh->qh;
       const double dh = *X.hubD;
       s[0] += X.pw[X.hub - X.wlo] * qh;
       s[1] += qh * (dh * X.rs[X.hub - X.r0]);
       s[2] += qh * (dh * qh);
-      if (lane == 0) sh->qh = qh;
     }
     if (lane < X.C) {
       const unsigned dst = cl_mapa(cl_smem_u32(&sh->cpart[X.par][X.rank][0]), lane);
       const unsigned rmb = cl_mapa(cl_smem_u32(mb), lane);
 #pragma unroll
-      for (int k = 0; k < NS; ++k) cl_st_async(dst + 8u * k, s[k], rmb);
+      for (int k = 0; k < ND; ++k) cl_st_async(dst + 8u * k, s[k], rmb);
     }
     cl_mbar_wait(mb, (X.red_phase >> X.par) & 1);
+    // rank-order sum: lane t holds CTA t's values, folded by the same fixed tree
 #pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      // rank-order sum: lane t holds CTA t's value, folded by a fixed tree
-      double w = lane < X.C ? sh->cpart[X.par][lane][k] : 0.0;
-#pragma unroll
-      for (int off = 8; off > 0; off >>= 1) w += __shfl_down_sync(0xffffffffu, w, off);
-      if (lane == 0) sh->tot[k] = w;
-    }
+    for (int k = 0; k < 8; ++k) v8[k] = (k < ND && lane < X.C) ? sh->cpart[X.par][lane][k] : 0.0;
+    const double tot = cl_butterfly8(v8, lane);
+    if ((lane & 3) == 0) sh->tot[cl_slot_of(lane)] = tot;
   }
   X.red_phase ^= 1 << X.par;
   X.par ^= 1;
@@ -193,16 +231,15 @@ __device__ __forceinline__ void cl_reduce(ClCtx& X, double (&v)[ND]) {
 // pointers of V), cluster totals {R.R, f.f, r.z, r.r}; publishes p.
 template <int NPE>
 __device__ __forceinline__ void cl_refill(ClCtx& X, const PropParams& P, const SysParams& S, const SbVec& V, int sys,
-                                          int step, bool first, unsigned pushmask, double (&t)[4]) {
+                                       int step, bool first, double (&t)[4]) {
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int i = X.r0 + threadIdx.x; i < X.r1; i += kClThreads)
     if (i != S.hub) sb_refill_row<NPE>(P, S, X.sh->curves, V, sys, step, first, i, acc);
   if (X.hub >= 0 && threadIdx.x == kClThreads - 1) sb_refill_hub<NPE>(P, S, X.sh->curves, V, sys, step, first, acc);
   if (X.sh->n_push) {
     __syncthreads();  // the hub row's p entry is written by another thread than the one that pushes it
-    int k = 0;
-    for (int i = X.r0 + threadIdx.x; i < X.r1; i += kClThreads, ++k)
-      if ((pushmask >> k) & 1u) cl_push_row(X, i, X.pw[i - X.wlo]);
+    for (int i = X.r0 + threadIdx.x; i < X.r1; i += kClThreads)
+      if (X.info[i - X.r0] & kClPush) cl_push_row(X, i, X.pw[i - X.wlo]);
   }
   cl_reduce<4, false>(X, acc);
   cl_halo_sync(X);
@@ -210,27 +247,9 @@ __device__ __forceinline__ void cl_refill(ClCtx& X, const PropParams& P, const S
   for (int k = 0; k < 4; ++k) t[k] = acc[k];
 }
 
-struct ClRow {
-  int c[kEll];
-  double a[kEll];
-  double dv;
-};
-
-// Operands of row i that stream from L2: padded columns, slot values (shared
-// M/dt + K_const or the system's own), Jacobi entry.
-__device__ __forceinline__ void cl_load_row(const PropParams& P, const SysParams& S, const SbVec& V, int i, bool own,
-                                            ClRow& o) {
-  const int d = P.d;
-  const double* As = own ? V.A : S.AshT;
-  const double* Ds = own ? V.D : P.Dsh;
-#pragma unroll
-  for (int k = 0; k < kEll; ++k) o.c[k] = __ldg(S.ciT + static_cast<size_t>(k) * d + i);
-#pragma unroll
-  for (int k = 0; k < kEll; ++k) o.a[k] = As[static_cast<size_t>(k) * d + i];
-  o.dv = Ds[i];
-}
-
-template <int NPE>
+// W: slots read per row = the longest row among the rows of <= kEll slots
+// (compile-time, so that the slot loops carry no predicates).
+template <int NPE, int W>
 __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropParams P, const SysParams S,
                                                                    const ClusterGeom Gm) {
   extern __shared__ __align__(16) unsigned char cl_smem[];
@@ -245,15 +264,20 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
   X.par = 0;
   X.red_phase = 0;
   X.halo_phase = 0;
-  X.pw = reinterpret_cast<double*>(cl_smem);
+  X.timed = P.dbg != nullptr;
+  X.sh = reinterpret_cast<ClShared*>(cl_smem);
+  X.pw = reinterpret_cast<double*>(cl_smem + sizeof(ClShared));
   X.rs = X.pw + Gm.win_max;
-  X.xs = X.rs + Gm.rows_max;
-  X.qs = X.xs + Gm.rows_max;
-  X.sh = reinterpret_cast<ClShared*>(X.qs + Gm.rows_max);
+  X.ds = X.rs + Gm.rows_max;
+  X.qs = X.ds + Gm.rows_max;
+  X.info = reinterpret_cast<unsigned short*>(X.qs + Gm.rows_max);
   ClShared* sh = X.sh;
   const int sys = blockIdx.x / Gm.C;
   const int tid = threadIdx.x;
   if (tid < P.ncurves) sh->curves[tid] = P.curves[tid];
+  for (int k = tid; k < kPatMax * (kEll / 4); k += kClThreads)
+    (&sh->pat_cols[0][0])[k] = __ldg(reinterpret_cast<const int4*>(S.pat_cols) + k);
+  for (int k = tid; k < kPatMax; k += kClThreads) sh->pat_meta[k] = __ldg(S.pat_meta + k);
   const int d = P.d;
   const int r0 = X.r0, r1 = X.r1;
   const size_t vb = static_cast<size_t>(sys) * d;
@@ -261,7 +285,7 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
   V.u = S.su + vb;
   V.uprev = P.uprev + vb;
   V.D = P.Dinv + vb;
-  V.x = X.xs - r0;
+  V.x = P.x + vb;
   V.r = X.rs - r0;
   V.p = X.pw - X.wlo;
   V.q = nullptr;
@@ -281,6 +305,7 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
     X.halo_in_bytes = in_bytes;
   }
   if (tid == 0) {
+    for (int k = 0; k < 4; ++k) sh->tm[k] = 0;
     cl_mbar_init(&sh->red_mb[0], 1);
     cl_mbar_init(&sh->red_mb[1], 1);
     cl_mbar_init(&sh->halo_mb, 1);
@@ -304,17 +329,33 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
   double* ub = P.u + static_cast<size_t>(g) * d * kLanes + l;
   for (int i = r0 + tid; i < r1; i += kClThreads) V.u[i] = ub[static_cast<size_t>(i) * kLanes];
   cl.sync();
-  // which of this thread's rows carry per-system values / are held by other windows
-  unsigned ownmask = 0, pushmask = 0;
-  {
-    int k = 0;
-    for (int i = r0 + tid; i < r1; i += kClThreads, ++k) {
-      if (!sb_shared_row(P, i)) ownmask |= 1u << k;
-      for (int e = 0; e < sh->n_push; ++e)
-        if (i >= sh->push_lo[e] && i < sh->push_hi[e]) pushmask |= 1u << k;
-    }
+  // per own row: pattern id (the hub row counts as irregular), whether its values
+  // are the system's own, whether other windows hold it
+  for (int i = r0 + tid; i < r1; i += kClThreads) {
+    unsigned v = i == S.hub ? static_cast<unsigned>(kPatIrregular) : __ldg(S.pat_id + i);
+    if (!sb_shared_row(P, i)) v |= kClOwn;
+    for (int e = 0; e < sh->n_push; ++e)
+      if (i >= sh->push_lo[e] && i < sh->push_hi[e]) v |= kClPush;
+    X.info[i - r0] = static_cast<unsigned short>(v);
   }
-
+  __syncthreads();
+  // the Jacobi entries of the CTA's rows after a refill (each thread its own rows)
+  auto load_jacobi = [&]() {
+    for (int i = r0 + tid; i < r1; i += kClThreads)
+      X.ds[i - r0] = (X.info[i - r0] & kClOwn) ? V.D[i] : __ldg(P.Dsh + i);
+  };
+  // hot-loop views: own rows by local index l = row - r0, p also by column
+  const int nloc = r1 - r0;
+  const int hubl = X.hub >= 0 ? X.hub - r0 : -1;
+  double* __restrict__ const rs = X.rs;
+  double* __restrict__ const ds = X.ds;
+  double* __restrict__ const qs = X.qs;
+  double* const pwo = X.pw + (r0 - X.wlo);
+  const double* const pw0 = X.pw - X.wlo;
+  const unsigned short* __restrict__ const info = X.info;
+  double* __restrict__ const xg = V.x + r0;   // x of own rows (global)
+  const double* __restrict__ const Aown = V.A + r0;
+  const double* __restrict__ const Ash = S.AshT + r0;
   const int hub_base = S.hub >= 0 ? __ldg(P.rp + S.hub) : 0;
   int code = PS_OK, last_nit = 0, max_nit = 0, max_pit = 0;
   double t_fail = 0.0, res_fail = 0.0;
@@ -322,7 +363,8 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
   double t[4];
   for (int step = 0; step < P.steps && code == PS_OK; ++step) {
     const double t_now = P.t_next[static_cast<size_t>(step) * P.count + sys];
-    cl_refill<NPE>(X, P, S, V, sys, step, true, pushmask, t);
+    cl_refill<NPE>(X, P, S, V, sys, step, true, t);
+    load_jacobi();
     const double tol = P.newton_tol_abs + P.newton_tol_rel * sqrt(t[1]);
     int nit = 1;
     double res_pre = sqrt(t[0]);
@@ -335,54 +377,90 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
         int pit = 0;
         for (;;) {
           // SpMV pass: q = A p over this thread's rows; partials p.q, q.z, q.Dq
-          // and r.z, r.r of the residual as the last update left it
-          double a6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-          {
-            int k = 0;
-#pragma unroll 1
-            for (int i0 = r0 + tid; i0 < r1; i0 += kClThreads * kClRb, k += kClRb) {
-              ClRow R[kClRb];
+          // and r.z, r.r of the residual as the last update left it.  Software
+          // pipeline: the slot values of the next kClRb rows are requested before
+          // the current kClRb rows are multiplied (all W slots of a row: pads hold
+          // 0 and point at the row itself; a row index past the range is clamped).
+          double a5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+          if (X.timed && tid == 0) sh->tm_c[0] = clock64();
+          double avA[kClRb][W], avB[kClRb][W];
+          unsigned infA[kClRb], infB[kClRb];
+          auto load_rows = [&](int l0, double (&av)[kClRb][W], unsigned (&inf)[kClRb]) {
 #pragma unroll
-              for (int u = 0; u < kClRb; ++u) {
-                const int i = i0 + u * kClThreads;
-                if (i < r1) cl_load_row(P, S, V, i, (ownmask >> (k + u)) & 1u, R[u]);
-              }
+            for (int u = 0; u < kClRb; ++u) {
+              const int l = min(l0 + u * kClThreads, nloc - 1);
+              inf[u] = info[l];
+              const double* ap = ((inf[u] & kClOwn) ? Aown : Ash) + l;
 #pragma unroll
-              for (int u = 0; u < kClRb; ++u) {
-                const int i = i0 + u * kClThreads;
-                if (i >= r1) break;
-                double qv = 0.0;
+              for (int s = 0; s < W; ++s) av[u][s] = ap[static_cast<size_t>(s) * d];
+            }
+          };
+          auto mult_rows = [&](int l0, const double (&av)[kClRb][W], const unsigned (&inf)[kClRb]) {
 #pragma unroll
-                for (int s = 0; s < kEll; ++s) qv += R[u].a[s] * X.pw[R[u].c[s] - X.wlo];
-                const double ri = X.rs[i - r0];
-                const double zi = R[u].dv * ri;
-                if (i != S.hub) {
-                  X.qs[i - r0] = qv;
-                  a6[0] += X.pw[i - X.wlo] * qv;
-                  a6[1] += qv * zi;
-                  a6[2] += qv * (R[u].dv * qv);
+            for (int u = 0; u < kClRb; ++u) {
+              const int l = l0 + u * kClThreads;
+              if (l >= nloc) break;
+              const unsigned pid = inf[u] & 0xffu;
+              const double ri = rs[l], dvi = ds[l];
+              const double zi = dvi * ri;
+              a5[3] += ri * zi;
+              a5[4] += ri * ri;
+              if (l == hubl) continue;   // the hub row's product comes from the last warp
+              const double* pwi = pwo + l;   // p at this row's own column
+              double qv = 0.0;
+              if (pid != static_cast<unsigned>(kPatIrregular)) {
+                const int4 o0 = sh->pat_cols[pid][0], o1 = sh->pat_cols[pid][1];
+                const int off[kEll] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+                const int absm = sh->pat_meta[pid] >> 8;
+                if (absm == 0) {
+#pragma unroll
+                  for (int s = 0; s < W; ++s) qv += av[u][s] * pwi[off[s]];
+                } else {
+                  // entries kept absolute (the hub's column)
+#pragma unroll
+                  for (int s = 0; s < W; ++s) qv += av[u][s] * (((absm >> s) & 1) ? pw0[off[s]] : pwi[off[s]]);
                 }
-                a6[3] += ri * zi;
-                a6[4] += ri * ri;
+              } else {
+                // outside the dictionary: padded columns from memory
+                const int* cp = S.ciT + (r0 + l);
+#pragma unroll
+                for (int s = 0; s < W; ++s) qv += av[u][s] * pw0[__ldg(cp + static_cast<size_t>(s) * d)];
               }
+              qs[l] = qv;
+              a5[0] += pwi[0] * qv;
+              a5[1] += qv * zi;
+              a5[2] += qv * (dvi * qv);
             }
+          };
+          constexpr int kStride = kClThreads * kClRb;
+          load_rows(tid, avA, infA);
+#pragma unroll 1
+          for (int l0 = tid; l0 < nloc; l0 += 2 * kStride) {
+            load_rows(l0 + kStride, avB, infB);
+            mult_rows(l0, avA, infA);
+            load_rows(l0 + 2 * kStride, avA, infA);
+            mult_rows(l0 + kStride, avB, infB);
           }
-          if (X.hub >= 0) {
-            // the hub row's product (its columns lie inside the owner's window)
+          if (X.hub >= 0 && (tid >> 5) == kClThreads / 32 - 1) {
+            // the hub row's product by the last warp (its columns lie inside the
+            // owner's window); the cluster sum folds it in
             double part = 0.0;
-            for (int s = tid; s < S.hub_len; s += kClThreads) {
+            for (int s = tid & 31; s < S.hub_len; s += 32) {
               const int kk = hub_base + s;
-              const double av = X.hub_shared ? __ldg(P.Ash + kk) : V.hA[s];
-              part += av * X.pw[__ldg(P.ci + kk) - X.wlo];
+              const double hv = X.hub_shared ? __ldg(P.Ash + kk) : V.hA[s];
+              part += hv * X.pw[__ldg(P.ci + kk) - X.wlo];
             }
-            a6[5] = part;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+            if ((tid & 31) == 0) sh->qh = part;
           }
-          cl_reduce<6, true>(X, a6);
-          const double t0v = a6[0], t1v = a6[1], t2v = a6[2];
+          cl_reduce<5, true>(X, a5);
+          if (X.timed && tid == 0) sh->tm_c[1] = clock64();
+          const double t0v = a5[0], t1v = a5[1], t2v = a5[2];
           if (pit > 0) {
             // the state after update `pit`
-            const double rr = a6[4];
-            rho = a6[3];
+            const double rr = a5[4];
+            rho = a5[3];
             if (rr <= stop) break;
             if (!isfinite(rr)) {
               code = PS_ERR_SINGULAR;
@@ -409,25 +487,47 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
           // update pass: x (+)= alpha p, r -= alpha q, z = D r, p = z + beta p
           const bool first_it = pit == 0;
           const double qh = X.hub >= 0 ? sh->qh : 0.0;
-          {
-            int k = 0;
-#pragma unroll 2
-            for (int i = r0 + tid; i < r1; i += kClThreads, ++k) {
-              const bool own = (ownmask >> k) & 1u;
-              const double dv = own ? V.D[i] : __ldg(P.Dsh + i);
-              const double pv = X.pw[i - X.wlo];
-              const double qv = i == S.hub ? qh : X.qs[i - r0];
-              const double xv = first_it ? 0.0 : X.xs[i - r0];
-              X.xs[i - r0] = first_it ? alpha * pv : xv + alpha * pv;
-              const double rn = X.rs[i - r0] - alpha * qv;
-              const double pn = dv * rn + beta * pv;
-              X.rs[i - r0] = rn;
-              X.pw[i - X.wlo] = pn;
-              if ((pushmask >> k) & 1u) cl_push_row(X, i, pn);
+          // x of this thread's rows (global, L2-resident): all requests first
+          double xr[kClRpt];
+#pragma unroll
+          for (int k = 0; k < kClRpt; ++k) {
+            const int l = min(tid + k * kClThreads, nloc - 1);
+            xr[k] = first_it ? 0.0 : xg[l];
+          }
+#pragma unroll
+          for (int kb = 0; kb < kClRpt; kb += 2) {
+            double pv[2], qv[2], rv[2], dv[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int l = min(tid + (kb + u) * kClThreads, nloc - 1);
+              pv[u] = pwo[l];
+              qv[u] = qs[l];
+              rv[u] = rs[l];
+              dv[u] = ds[l];
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int l = tid + (kb + u) * kClThreads;
+              if (kb + u < kClRpt && l < nloc) {
+                const double qq = l == hubl ? qh : qv[u];
+                xg[l] = xr[kb + u] + alpha * pv[u];
+                const double rn = rv[u] - alpha * qq;
+                const double pn = dv[u] * rn + beta * pv[u];
+                rs[l] = rn;
+                pwo[l] = pn;
+                if (info[l] & kClPush) cl_push_row(X, r0 + l, pn);
+              }
             }
           }
           pit += 1;
+          if (X.timed && tid == 0) sh->tm_c[2] = clock64();
           cl_halo_sync(X);
+          if (X.timed && tid == 0) {
+            sh->tm[0] += sh->tm_c[3] - sh->tm_c[0];
+            sh->tm[1] += sh->tm_c[1] - sh->tm_c[3];
+            sh->tm[2] += sh->tm_c[2] - sh->tm_c[1];
+            sh->tm[3] += clock64() - sh->tm_c[2];
+          }
         }
         if (code != PS_OK) break;
         pcg_total += pit;
@@ -455,7 +555,8 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
       // ---- residual at the trial point; optional backtracking
       double post;
       for (;;) {
-        cl_refill<NPE>(X, P, S, V, sys, step, false, pushmask, t);
+        cl_refill<NPE>(X, P, S, V, sys, step, false, t);
+        load_jacobi();
         post = sqrt(t[0]);
         if (P.line_search > 0 && ls_k < P.line_search && !(post <= tol) &&
             !(post <= (1.0 - 1e-4 * lambda) * res_pre)) {
@@ -509,6 +610,11 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
     o.max_pcg = max_pit;
     P.out[sys] = o;
     atomicMax(reinterpret_cast<unsigned long long*>(P.lockstep + g), static_cast<unsigned long long>(pcg_total));
+  }
+  if (X.timed && tid == 0) {
+    unsigned long long* o = P.dbg + (static_cast<size_t>(sys) * X.C + X.rank) * 8;
+    for (int k = 0; k < 4; ++k) o[k] = static_cast<unsigned long long>(sh->tm[k]);
+    o[4] = static_cast<unsigned long long>(pcg_total);
   }
   // no CTA may exit while others can still write into its shared memory
   cl.sync();

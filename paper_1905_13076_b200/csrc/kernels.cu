@@ -1924,23 +1924,36 @@ int launch_sysblock(const PropParams& prm, const SysParams& sp, int npe, cudaStr
 static_assert(kClMaxC == kClusterMaxC, "cluster geometry arrays");
 
 size_t syscluster_smem(const ClusterGeom& gm) {
-  return (static_cast<size_t>(gm.win_max) + 3 * static_cast<size_t>(gm.rows_max)) * sizeof(double) + sizeof(ClShared);
+  return (static_cast<size_t>(gm.win_max) + 3 * static_cast<size_t>(gm.rows_max)) * sizeof(double) +
+         static_cast<size_t>(gm.rows_max) * sizeof(unsigned short) + sizeof(ClShared) + 16;
 }
 
-int syscluster_max_rows() { return kClMaxRpt * kClThreads; }
+int syscluster_max_rows() { return kClRpt * kClThreads; }
 
 namespace {
-void* syscluster_fn(int npe) {
-  return npe == 2 ? reinterpret_cast<void*>(&syscluster_kernel<2>) : reinterpret_cast<void*>(&syscluster_kernel<3>);
+// instantiated slot widths: 3 (2-node radial elements), 7 (P1 triangles on the
+// polar mesh), kEll (anything else)
+int syscluster_width(int npe, int ell_width) {
+  if (npe == 2 && ell_width <= 3) return 3;
+  if (npe == 3 && ell_width <= 7) return 7;
+  return kEll;
 }
 
-bool syscluster_config(int npe, const ClusterGeom& gm, int count, cudaStream_t st, cudaLaunchConfig_t* cfg,
+using ClusterKernel = void (*)(const PropParams, const SysParams, const ClusterGeom);
+ClusterKernel syscluster_fn(int npe, int ell_width) {
+  const int w = syscluster_width(npe, ell_width);
+  if (npe == 2) return w == 3 ? syscluster_kernel<2, 3> : syscluster_kernel<2, kEll>;
+  return w == 7 ? syscluster_kernel<3, 7> : syscluster_kernel<3, kEll>;
+}
+
+bool syscluster_config(ClusterKernel fn, const ClusterGeom& gm, int count, cudaStream_t st, cudaLaunchConfig_t* cfg,
                        cudaLaunchAttribute* attr) {
-  void* fn = syscluster_fn(npe);
   const size_t smem = syscluster_smem(gm);
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
     return false;
-  if (gm.C > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+  if (gm.C > 8 && cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
     return false;
   *cfg = cudaLaunchConfig_t{};
   cfg->gridDim = dim3(static_cast<unsigned>(count) * gm.C);
@@ -1957,16 +1970,17 @@ bool syscluster_config(int npe, const ClusterGeom& gm, int count, cudaStream_t s
 }
 }  // namespace
 
-int syscluster_max_clusters(int npe, const ClusterGeom& gm) {
+int syscluster_max_clusters(int npe, int ell_width, const ClusterGeom& gm) {
   if (npe != 2 && npe != 3) return 0;
+  const ClusterKernel fn = syscluster_fn(npe, ell_width);
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr;
-  if (!syscluster_config(npe, gm, 1, nullptr, &cfg, &attr)) {
+  if (!syscluster_config(fn, gm, 1, nullptr, &cfg, &attr)) {
     cudaGetLastError();
     return 0;
   }
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, syscluster_fn(npe), &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(fn), &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -1976,14 +1990,14 @@ int syscluster_max_clusters(int npe, const ClusterGeom& gm) {
 int launch_syscluster(const PropParams& prm, const SysParams& sp, const ClusterGeom& gm, int npe, cudaStream_t st,
                       std::string* err) {
   if (npe != 2 && npe != 3) return PS_ERR_BAD_ARG;
+  const ClusterKernel fn = syscluster_fn(npe, sp.ell_width);
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr;
-  if (!syscluster_config(npe, gm, prm.count, st, &cfg, &attr)) {
+  if (!syscluster_config(fn, gm, prm.count, st, &cfg, &attr)) {
     if (err) *err = std::string("cuda: cluster engine setup failed: ") + cudaGetErrorString(cudaGetLastError());
     return PS_ERR_CUDA;
   }
-  const cudaError_t e = npe == 2 ? cudaLaunchKernelEx(&cfg, syscluster_kernel<2>, prm, sp, gm)
-                                 : cudaLaunchKernelEx(&cfg, syscluster_kernel<3>, prm, sp, gm);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, prm, sp, gm);
   if (e != cudaSuccess) {
     if (err) *err = std::string("cuda: cluster engine launch failed: ") + cudaGetErrorString(e);
     return PS_ERR_CUDA;

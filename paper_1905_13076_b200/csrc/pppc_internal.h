@@ -136,7 +136,16 @@ struct SysParams {
   int hub;              // the row longer than kEll, or -1
   int hub_len;
   int smem_vectors;     // 1: u, u_prev, x, r, p, q, Dinv in shared memory (7 d doubles)
+  // sparsity-pattern dictionary (cluster engine): row i's pattern id; pattern p's
+  // kEll column entries (relative to the row, or absolute where the bit of
+  // pat_meta's absolute mask is set) and pat_meta = length | absolute mask << 8
+  const unsigned char* pat_id;   // [d], kPatIrregular = not in the dictionary
+  const int* pat_cols;           // [kPatMax][kEll]
+  const int* pat_meta;           // [kPatMax]
+  int ell_width;                 // longest row among the rows of <= kEll slots
 };
+constexpr int kPatMax = 256;
+constexpr int kPatIrregular = kPatMax - 1;
 size_t sysblock_smem(int d);
 constexpr size_t kSbSmemMax = 200 * 1024;
 
@@ -191,7 +200,11 @@ struct DevProblem {
   // (every row <= kEll slots but at most one longer row)
   bool sb_ok = false;
   int sb_hub = -1;
+  int ell_width = 1;   // longest row among the rows of <= kEll slots
   int* ciT = nullptr;
+  unsigned char* pat_id = nullptr;
+  int* pat_cols = nullptr;
+  int* pat_meta = nullptr;
   double* MT = nullptr;
   double* KT = nullptr;
   std::vector<unsigned char> h_rowkind;
@@ -227,7 +240,7 @@ int launch_sysblock(const PropParams& prm, const SysParams& sp, int npe, cudaStr
 // co-resident clusters (0 = this geometry cannot launch), launch
 size_t syscluster_smem(const ClusterGeom& gm);
 int syscluster_max_rows();
-int syscluster_max_clusters(int npe, const ClusterGeom& gm);
+int syscluster_max_clusters(int npe, int ell_width, const ClusterGeom& gm);
 int launch_syscluster(const PropParams& prm, const SysParams& sp, const ClusterGeom& gm, int npe, cudaStream_t st,
                       std::string* err);
 
