@@ -377,7 +377,7 @@ void build_problem(ps_ctx* ctx, const ps_problem_desc* desc) {
       }
       // Sparsity-pattern dictionary for the cluster engine: a row's pattern is its
       // length and its columns relative to the row (the hub's column, which every
-      // neighbour of the hub holds, is kept absolute).  Structured meshes have a
+      // neighbour of the hub holds, is flagged absolute instead).  Structured meshes have a
       // handful of patterns; the kPatMax - 1 most frequent get an id, the other
       // rows stay "irregular" and read their padded columns from memory.
       std::map<std::vector<int>, int> freq;
@@ -388,8 +388,7 @@ void build_problem(ps_ctx* ctx, const ps_problem_desc* desc) {
         for (int k = 0; k < len; ++k) {
           const int c = P.h_ci[b + k];
           if (c == hub && c != i) {
-            absmask |= 1 << k;
-            key[2 + k] = c;
+            absmask |= 1 << k;   // the entry stays 0: the column is the hub
           } else {
             key[2 + k] = c - i;
           }

@@ -53,7 +53,10 @@ constexpr int kClRb = PPPC_CL_RB;     // rows per thread whose slot values are i
 constexpr int kClRpt = PPPC_CL_RPT;   // rows per thread at most (their x entries are registers)
 constexpr int kClMaxC = 16;           // CTAs per cluster at most (8 portable)
 constexpr int kClNd = 8;              // reduction slots per CTA
-constexpr unsigned kClOwn = 0x100u, kClPush = 0x200u;
+// per-row info word: pattern id | kClOwn (per-system values) | push entry + 1 in
+// bits 10..13 (kClPushMany: held by more than one other window)
+constexpr unsigned kClOwn = 0x100u, kClPushShift = 10u, kClPushMask = 0xfu << kClPushShift,
+                   kClPushMany = 0xfu;
 
 struct alignas(16) ClShared {
   int4 pat_cols[kPatMax][kEll / 4];       // pattern dictionary: column entries
@@ -83,7 +86,7 @@ struct ClCtx {
   double* rs;   // r of own rows (index = row - r0)
   double* ds;   // Jacobi entries of own rows
   double* qs;   // q of own rows
-  unsigned short* info;   // per own row: pattern id | kClOwn (per-system values) | kClPush (held by other windows)
+  unsigned short* info;   // per own row: pattern id | kClOwn | push entry (see kClPushShift)
   ClShared* sh;
   bool timed;          // PPPC_DEBUG_TIMING: thread 0 keeps cycle stamps in shared memory
 };
@@ -124,9 +127,14 @@ __device__ __forceinline__ void cl_mbar_wait(unsigned long long* mb, unsigned pa
   }
 }
 
-// Sends v (row i of p, owned here) to every CTA whose window holds column i.
-__device__ __forceinline__ void cl_push_row(const ClCtx& X, int i, double v) {
+// Sends v (row i of p, owned here) to the CTAs whose windows hold column i;
+// code = the row's push field (entry + 1, or kClPushMany: look the targets up).
+__device__ __forceinline__ void cl_push_row(const ClCtx& X, int i, double v, unsigned code) {
   const ClShared* sh = X.sh;
+  if (code != kClPushMany) {
+    cl_st_async(sh->push_base[code - 1] + static_cast<unsigned>(i) * 8u, v, sh->push_mb[code - 1]);
+    return;
+  }
   for (int e = 0; e < sh->n_push; ++e)
     if (i >= sh->push_lo[e] && i < sh->push_hi[e])
       cl_st_async(sh->push_base[e] + static_cast<unsigned>(i) * 8u, v, sh->push_mb[e]);
@@ -238,8 +246,10 @@ __device__ __forceinline__ void cl_refill(ClCtx& X, const PropParams& P, const S
   if (X.hub >= 0 && threadIdx.x == kClThreads - 1) sb_refill_hub<NPE>(P, S, X.sh->curves, V, sys, step, first, acc);
   if (X.sh->n_push) {
     __syncthreads();  // the hub row's p entry is written by another thread than the one that pushes it
-    for (int i = X.r0 + threadIdx.x; i < X.r1; i += kClThreads)
-      if (X.info[i - X.r0] & kClPush) cl_push_row(X, i, X.pw[i - X.wlo]);
+    for (int i = X.r0 + threadIdx.x; i < X.r1; i += kClThreads) {
+      const unsigned code = (X.info[i - X.r0] & kClPushMask) >> kClPushShift;
+      if (code) cl_push_row(X, i, X.pw[i - X.wlo], code);
+    }
   }
   cl_reduce<4, false>(X, acc);
   cl_halo_sync(X);
@@ -334,8 +344,10 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
   for (int i = r0 + tid; i < r1; i += kClThreads) {
     unsigned v = i == S.hub ? static_cast<unsigned>(kPatIrregular) : __ldg(S.pat_id + i);
     if (!sb_shared_row(P, i)) v |= kClOwn;
+    unsigned code = 0;
     for (int e = 0; e < sh->n_push; ++e)
-      if (i >= sh->push_lo[e] && i < sh->push_hi[e]) v |= kClPush;
+      if (i >= sh->push_lo[e] && i < sh->push_hi[e]) code = code ? kClPushMany : static_cast<unsigned>(e + 1);
+    v |= code << kClPushShift;
     X.info[i - r0] = static_cast<unsigned short>(v);
   }
   __syncthreads();
@@ -395,41 +407,66 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
               for (int s = 0; s < W; ++s) av[u][s] = ap[static_cast<size_t>(s) * d];
             }
           };
+          // Straight-line main path for all kClRb rows (so that their instructions
+          // interleave): every row is treated as a dictionary row without absolute
+          // entries, with a clamped index; the rare other rows are recomputed
+          // afterwards, and rows past the range / the hub row are masked out.
           auto mult_rows = [&](int l0, const double (&av)[kClRb][W], const unsigned (&inf)[kClRb]) {
+            double qv[kClRb], ri[kClRb], dvi[kClRb], pi[kClRb];
+            bool special[kClRb];
 #pragma unroll
             for (int u = 0; u < kClRb; ++u) {
-              const int l = l0 + u * kClThreads;
-              if (l >= nloc) break;
+              const int l = min(l0 + u * kClThreads, nloc - 1);
               const unsigned pid = inf[u] & 0xffu;
-              const double ri = rs[l], dvi = ds[l];
-              const double zi = dvi * ri;
-              a5[3] += ri * zi;
-              a5[4] += ri * ri;
-              if (l == hubl) continue;   // the hub row's product comes from the last warp
+              const int4 o0 = sh->pat_cols[pid][0], o1 = sh->pat_cols[pid][1];
+              const int off[kEll] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+              special[u] = pid == static_cast<unsigned>(kPatIrregular) || (sh->pat_meta[pid] >> 8) != 0;
               const double* pwi = pwo + l;   // p at this row's own column
-              double qv = 0.0;
+              ri[u] = rs[l];
+              dvi[u] = ds[l];
+              pi[u] = pwi[0];
+              // two partial sums (even / odd slots) shorten the dependent chain
+              double qe = 0.0, qo = 0.0;
+#pragma unroll
+              for (int s = 0; s < W; s += 2) qe += av[u][s] * pwi[off[s]];
+#pragma unroll
+              for (int s = 1; s < W; s += 2) qo += av[u][s] * pwi[off[s]];
+              qv[u] = qe + qo;
+            }
+#pragma unroll
+            for (int u = 0; u < kClRb; ++u) {
+              if (!special[u]) continue;
+              const int l = min(l0 + u * kClThreads, nloc - 1);
+              const unsigned pid = inf[u] & 0xffu;
+              double q = 0.0;
               if (pid != static_cast<unsigned>(kPatIrregular)) {
+                // dictionary row with entries kept absolute (the hub's column)
                 const int4 o0 = sh->pat_cols[pid][0], o1 = sh->pat_cols[pid][1];
                 const int off[kEll] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
                 const int absm = sh->pat_meta[pid] >> 8;
-                if (absm == 0) {
 #pragma unroll
-                  for (int s = 0; s < W; ++s) qv += av[u][s] * pwi[off[s]];
-                } else {
-                  // entries kept absolute (the hub's column)
-#pragma unroll
-                  for (int s = 0; s < W; ++s) qv += av[u][s] * (((absm >> s) & 1) ? pw0[off[s]] : pwi[off[s]]);
-                }
+                for (int s = 0; s < W; ++s) q += av[u][s] * (((absm >> s) & 1) ? pw0[S.hub] : pwo[l + off[s]]);
               } else {
                 // outside the dictionary: padded columns from memory
                 const int* cp = S.ciT + (r0 + l);
 #pragma unroll
-                for (int s = 0; s < W; ++s) qv += av[u][s] * pw0[__ldg(cp + static_cast<size_t>(s) * d)];
+                for (int s = 0; s < W; ++s) q += av[u][s] * pw0[__ldg(cp + static_cast<size_t>(s) * d)];
               }
-              qs[l] = qv;
-              a5[0] += pwi[0] * qv;
-              a5[1] += qv * zi;
-              a5[2] += qv * (dvi * qv);
+              qv[u] = q;
+            }
+#pragma unroll
+            for (int u = 0; u < kClRb; ++u) {
+              const int l = l0 + u * kClThreads;
+              const bool in = l < nloc;
+              const bool mul = in && l != hubl;   // the hub row's product comes from the last warp
+              const double r = in ? ri[u] : 0.0, q = mul ? qv[u] : 0.0;
+              const double zi = dvi[u] * r;
+              if (mul) qs[l] = q;
+              a5[0] += pi[u] * q;
+              a5[1] += q * zi;
+              a5[2] += q * (dvi[u] * q);
+              a5[3] += r * zi;
+              a5[4] += r * r;
             }
           };
           constexpr int kStride = kClThreads * kClRb;
@@ -487,36 +524,42 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
           // update pass: x (+)= alpha p, r -= alpha q, z = D r, p = z + beta p
           const bool first_it = pit == 0;
           const double qh = X.hub >= 0 ? sh->qh : 0.0;
-          // x of this thread's rows (global, L2-resident): all requests first
-          double xr[kClRpt];
+          // rows in batches of four; x (global, L2-resident) of the next batch is
+          // requested before the current batch is updated
+          {
+            constexpr int kB = 4;
+            double xa[kB], xn[kB];
 #pragma unroll
-          for (int k = 0; k < kClRpt; ++k) {
-            const int l = min(tid + k * kClThreads, nloc - 1);
-            xr[k] = first_it ? 0.0 : xg[l];
-          }
+            for (int u = 0; u < kB; ++u) xa[u] = first_it ? 0.0 : xg[min(tid + u * kClThreads, nloc - 1)];
+#pragma unroll 1
+            for (int l0 = tid; l0 < nloc; l0 += kB * kClThreads) {
 #pragma unroll
-          for (int kb = 0; kb < kClRpt; kb += 2) {
-            double pv[2], qv[2], rv[2], dv[2];
+              for (int u = 0; u < kB; ++u)
+                xn[u] = first_it ? 0.0 : xg[min(l0 + (kB + u) * kClThreads, nloc - 1)];
+              double pv[kB], qq[kB], rv[kB], dv[kB];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int l = min(tid + (kb + u) * kClThreads, nloc - 1);
-              pv[u] = pwo[l];
-              qv[u] = qs[l];
-              rv[u] = rs[l];
-              dv[u] = ds[l];
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int l = tid + (kb + u) * kClThreads;
-              if (kb + u < kClRpt && l < nloc) {
-                const double qq = l == hubl ? qh : qv[u];
-                xg[l] = xr[kb + u] + alpha * pv[u];
-                const double rn = rv[u] - alpha * qq;
-                const double pn = dv[u] * rn + beta * pv[u];
-                rs[l] = rn;
-                pwo[l] = pn;
-                if (info[l] & kClPush) cl_push_row(X, r0 + l, pn);
+              for (int u = 0; u < kB; ++u) {
+                const int l = min(l0 + u * kClThreads, nloc - 1);
+                pv[u] = pwo[l];
+                qq[u] = l == hubl ? qh : qs[l];
+                rv[u] = rs[l];
+                dv[u] = ds[l];
               }
+#pragma unroll
+              for (int u = 0; u < kB; ++u) {
+                const int l = l0 + u * kClThreads;
+                const double rn = rv[u] - alpha * qq[u];
+                const double pn = dv[u] * rn + beta * pv[u];
+                if (l < nloc) {
+                  xg[l] = xa[u] + alpha * pv[u];
+                  rs[l] = rn;
+                  pwo[l] = pn;
+                  const unsigned code = (info[l] & kClPushMask) >> kClPushShift;
+                  if (code) cl_push_row(X, r0 + l, pn, code);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < kB; ++u) xa[u] = xn[u];
             }
           }
           pit += 1;

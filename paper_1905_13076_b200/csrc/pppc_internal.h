@@ -137,8 +137,8 @@ struct SysParams {
   int hub_len;
   int smem_vectors;     // 1: u, u_prev, x, r, p, q, Dinv in shared memory (7 d doubles)
   // sparsity-pattern dictionary (cluster engine): row i's pattern id; pattern p's
-  // kEll column entries (relative to the row, or absolute where the bit of
-  // pat_meta's absolute mask is set) and pat_meta = length | absolute mask << 8
+  // kEll column entries (relative to the row; 0 where the bit of pat_meta's
+  // absolute mask is set: that column is the hub) and pat_meta = length | absolute mask << 8
   const unsigned char* pat_id;   // [d], kPatIrregular = not in the dictionary
   const int* pat_cols;           // [kPatMax][kEll]
   const int* pat_meta;           // [kPatMax]
