@@ -150,17 +150,18 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(args):
-    """DRAM bytes (read + write) per launch of the persistent kernel from the
-    committed ncu capture of this same default command (profiles/ncu_traffic.json);
-    None for any other workload."""
+def ncu_traffic(args, engine="lane"):
+    """DRAM bytes (read + write) per launch of the propagation kernel from the
+    committed ncu capture of this same default command (profiles/ncu_traffic.json,
+    one entry per engine); None for any other workload."""
     default = (args.nr, args.ntheta, args.subintervals, args.fine_steps, args.pcg_tol) == (200, 256, 100, 20, 1e-12)
     if not default:
         return None
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    key = {"lane": "config2", "cluster": "config2_cluster"}.get(engine)
     try:
         with open(path) as f:
-            return float(json.load(f)["config2"]["dram_bytes_per_launch"])
+            return float(json.load(f)[key]["dram_bytes_per_launch"])
     except Exception:
         return None
 
@@ -374,9 +375,10 @@ def run_ours(args):
         barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     # per step: one blocked-layout transpose per 32-system group in, the
-    # persistent propagation kernel, one transpose per group out
+    # propagation kernel, one transpose per group out
     groups = (N + 31) // 32
     launches = (2 * groups + 1) * args.steps
+    eng = prop.last_engine()
 
     # e2e: the public host-array API, H2D of the start states and D2H of F inside
     barrier()
@@ -405,7 +407,11 @@ def run_ours(args):
             dist.destroy_process_group()
         return 0
     last = statuses[-1]
-    traffic = ncu_traffic(args)
+    traffic = ncu_traffic(args, eng["engine"])
+    kernels = {"lane": "propagate_kernel<false,3> (persistent Newton + Jacobi-PCG, vectors in HBM)",
+               "block": "sysblock_kernel<3,512> (one block per system)",
+               "cluster": "syscluster_kernel<3,7> (one thread-block cluster per system: Newton + Jacobi-PCG with "
+                          "the Krylov vectors in the cluster's shared memory, matrix values streamed from L2)"}
     cfg = config_dict(args, prob)
     if world > 1:
         cfg["parallelism"] = f"{world} GPU(s) x {N} subintervals each (independent fine propagators)"
@@ -419,9 +425,10 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "frac_vs_nominal_8000": achieved / 8000.0,
                      "dram_gbs_measured": (traffic / (kernel_ms / 1e3) / 1e9) if traffic else None,
-                     "kernel": "propagate_kernel<false,3> (persistent Newton + Jacobi-PCG)",
+                     "kernel": kernels.get(eng["engine"], eng["engine"]),
                      "peak_source": peak_src,
                      "bytes_per_launch": bytes_per_launch, "kernel_ms": kernel_ms},
+        "engine": eng,
         "solver": {"newton_iterations": last["newton_iterations"], "pcg_iterations": last["pcg_iterations"],
                    "lockstep_pcg_iterations": last["lockstep_pcg_iterations"],
                    "max_pcg_per_solve": last["max_pcg_iterations"],
@@ -429,6 +436,20 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     line["solver"]["newton_per_system_step"] = last["newton_iterations"] / (N * s)
+    if eng["engine"] == "cluster":
+        # The canonical bytes (8 nnz + 80 d per PCG iteration) assume
+        # the Krylov vectors and the pattern stream from HBM; this engine keeps them
+        # on chip, so the HBM fraction can exceed 1.  What it does stream per PCG
+        # iteration and system comes from L2: the slot values (7 x 8 d, shared or
+        # per-system) and x (16 d); L2 peak = the 6300 B/clk LTS cap of
+        # /opt/skills/guides/B300_MICROARCH.md at the sampled SM clock.
+        l2_bytes = last["pcg_iterations"] * (7 * 8 + 16) * d
+        l2_peak = 6300.0 * line["clocks"]["sm_mhz"] * 1e6 / 1e9 if line["clocks"].get("sm_mhz") else None
+        l2_gbs = l2_bytes / (kernel_ms / 1e3) / 1e9
+        line["roofline"]["on_chip"] = {
+            "note": "operands resident in shared memory / L2; DRAM traffic is the ncu figure in `traffic`",
+            "l2_streamed_bytes_per_launch": l2_bytes, "l2_achieved_gbs": l2_gbs, "l2_peak_gbs": l2_peak,
+            "l2_frac": (l2_gbs / l2_peak) if l2_peak else None}
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args)

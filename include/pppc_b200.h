@@ -189,6 +189,10 @@ int ps_create(const ps_problem_desc* problem, const ps_time_mesh* mesh,
               const ps_solver_settings* settings, void* stream, ps_ctx** out);
 void ps_destroy(ps_ctx* ctx);
 const char* ps_last_error(const ps_ctx* ctx);
+/* Which engine ran the context's last propagation (1 lane, 2 block, 3 cluster; 0 =
+ * none yet) and, for the cluster engine, the CTAs per cluster and the clusters
+ * the device holds at once.  Diagnostics for the bench line; any pointer may be NULL. */
+int ps_last_engine(const ps_ctx* ctx, int32_t* engine, int32_t* cluster_ctas, int32_t* coresident_clusters);
 /* Error string for failures that happen before a context exists. */
 const char* ps_global_error(void);
 int ps_dim(const ps_ctx* ctx);

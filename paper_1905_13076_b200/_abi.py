@@ -124,6 +124,7 @@ _SIGNATURES = {
                             C.POINTER(ps_solver_settings), vp, C.POINTER(vp)]),
     "ps_destroy": (None, [vp]),
     "ps_last_error": (C.c_char_p, [vp]),
+    "ps_last_engine": (C.c_int, [vp, ip, ip, ip]),
     "ps_global_error": (C.c_char_p, []),
     "ps_dim": (C.c_int, [vp]),
     "ps_is_linear": (C.c_int, [vp]),

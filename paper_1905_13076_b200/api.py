@@ -436,7 +436,7 @@ class Propagator:
         if _ctx is not None:
             self._ctx = _ctx
             return
-        # engine: 0 by size, 1 lane engine, 2 block engine (ps_solver_settings.engine)
+        # engine: 0 by size, 1 lane engine, 2 block engine, 3 cluster engine (ps_solver_settings.engine)
         self._settings = solver_settings(self.newton, self.pcg, self.cocg, max_batch, engine)
         ctx = C.c_void_p()
         m = mesh.c()
@@ -459,6 +459,14 @@ class Propagator:
     @property
     def dim(self) -> int:
         return self.problem.dim
+
+    def last_engine(self) -> dict:
+        """ps_last_engine: which engine ran the last propagation (lane / block /
+        cluster) and the cluster geometry."""
+        e, c, n = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+        _raise(lib().ps_last_engine(self._ctx, C.byref(e), C.byref(c), C.byref(n)))
+        return {"engine": {0: "none", 1: "lane", 2: "block", 3: "cluster"}[e.value],
+                "cluster_ctas": c.value, "coresident_clusters": n.value}
 
     def _check(self, rc):
         _raise(rc, self._ctx)

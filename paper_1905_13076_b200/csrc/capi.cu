@@ -133,6 +133,7 @@ struct ps_ctx {
   ClusterGeom cl_geo{};
   int cl_slots = 0;       // co-resident clusters
   bool cl_sized = false;
+  int last_engine = 0;    // 1 lane, 2 block, 3 cluster (ps_last_engine)
   SpectralState* spec = nullptr;
   int spec_N = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -784,6 +785,7 @@ PropResult propagate(ps_ctx* ctx, int count, int steps, double dt, const std::ve
   const int nblk = geo.G * geo.C;
   const Engine engine = select_engine(ctx, linear_path, probe_refill);
   const bool sysblock = engine != Engine::Lane;
+  ctx->last_engine = engine == Engine::Lane ? 1 : engine == Engine::Block ? 2 : 3;
   if (debug_timing && !sysblock && dalloc(&dbg, static_cast<size_t>(nblk) * kDbgSlots)) K.dbg = dbg;
   unsigned long long* cl_dbg = nullptr;
   if (debug_timing && engine == Engine::Cluster &&
@@ -1174,6 +1176,14 @@ void ps_destroy(ps_ctx* ctx) {
 }
 
 const char* ps_last_error(const ps_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_error.c_str(); }
+
+int ps_last_engine(const ps_ctx* ctx, int32_t* engine, int32_t* cluster_ctas, int32_t* coresident_clusters) {
+  if (!ctx) return PS_ERR_BAD_ARG;
+  if (engine) *engine = ctx->last_engine;
+  if (cluster_ctas) *cluster_ctas = ctx->last_engine == 3 ? ctx->cl_geo.C : 0;
+  if (coresident_clusters) *coresident_clusters = ctx->last_engine == 3 ? ctx->cl_slots : 0;
+  return PS_OK;
+}
 int ps_dim(const ps_ctx* ctx) { return ctx ? ctx->P.d : -1; }
 int ps_is_linear(const ps_ctx* ctx) { return ctx && ctx->P.linear ? 1 : 0; }
 
