@@ -635,7 +635,7 @@ Engine select_engine(ps_ctx* ctx, bool linear_path, bool probe_refill) {
   const int e = ctx->settings.engine;
   if (e == 1) return Engine::Lane;
   if (e == 2) return Engine::Block;
-  static const char* env = std::getenv("PPPC_ENGINE");
+  const char* env = std::getenv("PPPC_ENGINE");
   if (e == 0 && env && std::strcmp(env, "lane") == 0) return Engine::Lane;
   if (e == 0 && env && std::strcmp(env, "sys") == 0) return Engine::Block;
   const bool want_cluster = e == 3 || (env && std::strcmp(env, "cluster") == 0);

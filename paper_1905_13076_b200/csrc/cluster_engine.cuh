@@ -49,7 +49,11 @@ namespace cg = cooperative_groups;
 #define PPPC_CL_RPT (6656 / PPPC_CL_THREADS)
 #endif
 constexpr int kClThreads = PPPC_CL_THREADS;
-constexpr int kClRb = PPPC_CL_RB;     // rows per thread whose slot values are in flight together (SpMV pass)
+constexpr int kClRb = PPPC_CL_RB;     // rows per thread whose slot values are requested together (SpMV pass)
+#ifndef PPPC_CL_PIPE
+#define PPPC_CL_PIPE 1
+#endif
+constexpr int kClPipe = PPPC_CL_PIPE; // groups of kClRb rows requested ahead of the one being multiplied (0, 1, 2)
 constexpr int kClRpt = PPPC_CL_RPT;   // rows per thread at most (their x entries are registers)
 constexpr int kClMaxC = 16;           // CTAs per cluster at most (8 portable)
 constexpr int kClNd = 8;              // reduction slots per CTA
@@ -395,8 +399,8 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
           // 0 and point at the row itself; a row index past the range is clamped).
           double a5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
           if (X.timed && tid == 0) sh->tm_c[0] = clock64();
-          double avA[kClRb][W], avB[kClRb][W];
-          unsigned infA[kClRb], infB[kClRb];
+          double avA[kClRb][W], avB[kClRb][W], avC[kClRb][W];
+          unsigned infA[kClRb], infB[kClRb], infC[kClRb];
           auto load_rows = [&](int l0, double (&av)[kClRb][W], unsigned (&inf)[kClRb]) {
 #pragma unroll
             for (int u = 0; u < kClRb; ++u) {
@@ -470,13 +474,38 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
             }
           };
           constexpr int kStride = kClThreads * kClRb;
-          load_rows(tid, avA, infA);
+          if (kClPipe == 0) {
+            // no pipeline: the rows' values are requested, then multiplied
+            (void)avB, (void)avC, (void)infB, (void)infC;
 #pragma unroll 1
-          for (int l0 = tid; l0 < nloc; l0 += 2 * kStride) {
-            load_rows(l0 + kStride, avB, infB);
-            mult_rows(l0, avA, infA);
-            load_rows(l0 + 2 * kStride, avA, infA);
-            mult_rows(l0 + kStride, avB, infB);
+            for (int l0 = tid; l0 < nloc; l0 += kStride) {
+              load_rows(l0, avA, infA);
+              mult_rows(l0, avA, infA);
+            }
+          } else if (kClPipe == 1) {
+            // one group of rows ahead (two register buffers)
+            (void)avC, (void)infC;
+            load_rows(tid, avA, infA);
+#pragma unroll 1
+            for (int l0 = tid; l0 < nloc; l0 += 2 * kStride) {
+              load_rows(l0 + kStride, avB, infB);
+              mult_rows(l0, avA, infA);
+              load_rows(l0 + 2 * kStride, avA, infA);
+              mult_rows(l0 + kStride, avB, infB);
+            }
+          } else {
+            // two groups of rows ahead (three register buffers)
+            load_rows(tid, avA, infA);
+            load_rows(tid + kStride, avB, infB);
+#pragma unroll 1
+            for (int l0 = tid; l0 < nloc; l0 += 3 * kStride) {
+              load_rows(l0 + 2 * kStride, avC, infC);
+              mult_rows(l0, avA, infA);
+              load_rows(l0 + 3 * kStride, avA, infA);
+              mult_rows(l0 + kStride, avB, infB);
+              load_rows(l0 + 4 * kStride, avB, infB);
+              mult_rows(l0 + 2 * kStride, avC, infC);
+            }
           }
           if (X.hub >= 0 && (tid >> 5) == kClThreads / 32 - 1) {
             // the hub row's product by the last warp (its columns lie inside the

