@@ -53,6 +53,10 @@ constexpr int kClRb = PPPC_CL_RB;     // rows per thread whose slot values are r
 #ifndef PPPC_CL_PIPE
 #define PPPC_CL_PIPE 1
 #endif
+#ifndef PPPC_CL_EXP
+#define PPPC_CL_EXP 0   // timing experiments only (results are wrong): 1 no x traffic, 2 slot values not read, 4 p not gathered
+#endif
+constexpr int kClExp = PPPC_CL_EXP;
 constexpr int kClPipe = PPPC_CL_PIPE; // groups of kClRb rows requested ahead of the one being multiplied (0, 1, 2)
 constexpr int kClRpt = PPPC_CL_RPT;   // rows per thread at most (their x entries are registers)
 constexpr int kClMaxC = 16;           // CTAs per cluster at most (8 portable)
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
               inf[u] = info[l];
               const double* ap = ((inf[u] & kClOwn) ? Aown : Ash) + l;
 #pragma unroll
-              for (int s = 0; s < W; ++s) av[u][s] = ap[static_cast<size_t>(s) * d];
+              for (int s = 0; s < W; ++s) av[u][s] = (kClExp & 2) ? 1.0 + s : ap[static_cast<size_t>(s) * d];
             }
           };
           // Straight-line main path for all kClRb rows (so that their instructions
@@ -432,9 +436,9 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
               // two partial sums (even / odd slots) shorten the dependent chain
               double qe = 0.0, qo = 0.0;
 #pragma unroll
-              for (int s = 0; s < W; s += 2) qe += av[u][s] * pwi[off[s]];
+              for (int s = 0; s < W; s += 2) qe += av[u][s] * ((kClExp & 4) ? pi[u] + off[s] : pwi[off[s]]);
 #pragma unroll
-              for (int s = 1; s < W; s += 2) qo += av[u][s] * pwi[off[s]];
+              for (int s = 1; s < W; s += 2) qo += av[u][s] * ((kClExp & 4) ? pi[u] + off[s] : pwi[off[s]]);
               qv[u] = qe + qo;
             }
 #pragma unroll
@@ -559,12 +563,13 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
             constexpr int kB = 4;
             double xa[kB], xn[kB];
 #pragma unroll
-            for (int u = 0; u < kB; ++u) xa[u] = first_it ? 0.0 : xg[min(tid + u * kClThreads, nloc - 1)];
+            for (int u = 0; u < kB; ++u)
+              xa[u] = (first_it || (kClExp & 1)) ? 0.0 : xg[min(tid + u * kClThreads, nloc - 1)];
 #pragma unroll 1
             for (int l0 = tid; l0 < nloc; l0 += kB * kClThreads) {
 #pragma unroll
               for (int u = 0; u < kB; ++u)
-                xn[u] = first_it ? 0.0 : xg[min(l0 + (kB + u) * kClThreads, nloc - 1)];
+                xn[u] = (first_it || (kClExp & 1)) ? 0.0 : xg[min(l0 + (kB + u) * kClThreads, nloc - 1)];
               double pv[kB], qq[kB], rv[kB], dv[kB];
 #pragma unroll
               for (int u = 0; u < kB; ++u) {
@@ -580,7 +585,7 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
                 const double rn = rv[u] - alpha * qq[u];
                 const double pn = dv[u] * rn + beta * pv[u];
                 if (l < nloc) {
-                  xg[l] = xa[u] + alpha * pv[u];
+                  if (!(kClExp & 1) || l == 0) xg[l] = xa[u] + alpha * pv[u];
                   rs[l] = rn;
                   pwo[l] = pn;
                   const unsigned code = (info[l] & kClPushMask) >> kClPushShift;

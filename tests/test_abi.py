@@ -44,6 +44,12 @@ def test_default_settings_are_reference_defaults():
     assert s.newton.line_search == 0
 
 
+def test_last_engine_needs_a_context():
+    e = C.c_int32(-1)
+    assert _abi.lib().ps_last_engine(None, C.byref(e), None, None) == _abi.PS_ERR_BAD_ARG
+    assert e.value == -1
+
+
 def _has_gpu():
     name = C.create_string_buffer(64)
     return _abi.lib().ps_device_info(name, 64, None, None, None) == 0
