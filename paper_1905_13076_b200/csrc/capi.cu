@@ -566,6 +566,7 @@ struct PropResult {
 ClusterGeom cluster_split(const DevProblem& P, int C) {
   ClusterGeom g{};
   g.C = C;
+  g.hub_len = P.sb_hub >= 0 ? P.h_rp[P.sb_hub + 1] - P.h_rp[P.sb_hub] : 0;
   for (int c = 0; c <= C; ++c) g.row_begin[c] = static_cast<int>(static_cast<int64_t>(P.d) * c / C);
   for (int c = 0; c < C; ++c) {
     const int r0 = g.row_begin[c], r1 = g.row_begin[c + 1];

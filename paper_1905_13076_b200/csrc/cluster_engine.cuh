@@ -289,6 +289,9 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
   X.ds = X.rs + Gm.rows_max;
   X.qs = X.ds + Gm.rows_max;
   X.info = reinterpret_cast<unsigned short*>(X.qs + Gm.rows_max);
+  // the hub row's values and window indices (owner CTA), 8-byte aligned after the info words
+  double* const hubv = reinterpret_cast<double*>(X.info + ((Gm.rows_max + 3) & ~3));
+  int* const hubc = reinterpret_cast<int*>(hubv + Gm.hub_len);
   ClShared* sh = X.sh;
   const int sys = blockIdx.x / Gm.C;
   const int tid = threadIdx.x;
@@ -359,10 +362,19 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
     X.info[i - r0] = static_cast<unsigned short>(v);
   }
   __syncthreads();
+  const int hub_base = S.hub >= 0 ? __ldg(P.rp + S.hub) : 0;
+  if (X.hub >= 0)
+    for (int s = tid; s < S.hub_len; s += kClThreads) hubc[s] = __ldg(P.ci + hub_base + s) - X.wlo;
   // the Jacobi entries of the CTA's rows after a refill (each thread its own rows)
+  // ... and the hub row's slot values (its owner; the last warp multiplies them)
   auto load_jacobi = [&]() {
     for (int i = r0 + tid; i < r1; i += kClThreads)
       X.ds[i - r0] = (X.info[i - r0] & kClOwn) ? V.D[i] : __ldg(P.Dsh + i);
+    if (X.hub >= 0) {
+      for (int s = tid; s < S.hub_len; s += kClThreads)
+        hubv[s] = X.hub_shared ? __ldg(P.Ash + hub_base + s) : V.hA[s];
+      __syncthreads();
+    }
   };
   // hot-loop views: own rows by local index l = row - r0, p also by column
   const int nloc = r1 - r0;
@@ -376,7 +388,6 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
   double* __restrict__ const xg = V.x + r0;   // x of own rows (global)
   const double* __restrict__ const Aown = V.A + r0;
   const double* __restrict__ const Ash = S.AshT + r0;
-  const int hub_base = S.hub >= 0 ? __ldg(P.rp + S.hub) : 0;
   int code = PS_OK, last_nit = 0, max_nit = 0, max_pit = 0;
   double t_fail = 0.0, res_fail = 0.0;
   long long newton_total = 0, pcg_total = 0;
@@ -515,11 +526,7 @@ __global__ void __launch_bounds__(kClThreads, 1) syscluster_kernel(const PropPar
             // the hub row's product by the last warp (its columns lie inside the
             // owner's window); the cluster sum folds it in
             double part = 0.0;
-            for (int s = tid & 31; s < S.hub_len; s += 32) {
-              const int kk = hub_base + s;
-              const double hv = X.hub_shared ? __ldg(P.Ash + kk) : V.hA[s];
-              part += hv * X.pw[__ldg(P.ci + kk) - X.wlo];
-            }
+            for (int s = tid & 31; s < S.hub_len; s += 32) part += hubv[s] * X.pw[hubc[s]];
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
             if ((tid & 31) == 0) sh->qh = part;

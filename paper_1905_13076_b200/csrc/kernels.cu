@@ -1925,7 +1925,8 @@ static_assert(kClMaxC == kClusterMaxC, "cluster geometry arrays");
 
 size_t syscluster_smem(const ClusterGeom& gm) {
   return (static_cast<size_t>(gm.win_max) + 3 * static_cast<size_t>(gm.rows_max)) * sizeof(double) +
-         static_cast<size_t>(gm.rows_max) * sizeof(unsigned short) + sizeof(ClShared) + 16;
+         static_cast<size_t>((gm.rows_max + 3) & ~3) * sizeof(unsigned short) +
+         static_cast<size_t>(gm.hub_len) * (sizeof(double) + sizeof(int)) + sizeof(ClShared) + 16;
 }
 
 int syscluster_max_rows() { return kClRpt * kClThreads; }

@@ -158,6 +158,7 @@ struct ClusterGeom {
   int C;
   int rows_max;   // largest row range
   int win_max;    // largest window
+  int hub_len;    // slots of the hub row (0 = none): its values and window indices sit in shared memory
   int row_begin[kClusterMaxC + 1];
   int win_lo[kClusterMaxC];
   int win_hi[kClusterMaxC];
