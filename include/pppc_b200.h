@@ -157,11 +157,11 @@ typedef struct {
   ps_krylov_settings pcg;   /* Jacobi-PCG for every step system (replaces SimplicialLDLT) */
   ps_krylov_settings cocg;  /* Jacobi-COCG per harmonic block (replaces complex SparseLU) */
   int32_t max_batch;        /* systems resident per batch (0 = subintervals) */
-  int32_t engine;           /* fine batches of nonlinear element problems: 0 = by size (one block per
-                               system when its vectors fit in one block's shared memory, one
-                               thread-block cluster per system when they fit in a cluster's, else
-                               one warp lane per system), 1 = lane engine, 2 = block engine,
-                               3 = cluster engine */
+  int32_t engine;           /* fine batches of nonlinear element problems: 0 = by size (one
+                               thread-block cluster per system when its vectors fit in a cluster's
+                               shared memory, else one block per system when they fit in one
+                               block's, else one warp lane per system), 1 = lane engine,
+                               2 = block engine, 3 = cluster engine */
 } ps_solver_settings;
 
 /* Outcome of one batched call.  On error `code` != PS_OK and `failed_index`

@@ -585,10 +585,17 @@ ClusterGeom cluster_split(const DevProblem& P, int C) {
   return g;
 }
 
-// Picks the cluster size: every C whose CTA working set (p window, r, x, q) fits in
-// shared memory and whose row range fits the per-thread row masks; among
-// them the one that keeps most SMs busy (C x co-resident clusters), the smaller
-// C on ties.  PPPC_CLUSTER=C forces a size.
+// Picks the cluster size among every C whose CTA working set (p window, r, q,
+// Jacobi) fits in shared memory and whose row range fits the per-thread row
+// budget.  A system runs roughly C times faster on C CTAs and the context's batch
+// (max_batch systems) takes ceil(max_batch / co-resident clusters) waves, so the
+// score is C * max_batch / waves: configs[1] (100 systems, d = 50,945) -> C = 9
+// (15 clusters at once, the only sizes that fit are 9..16); configs[0] (20 systems,
+// d = 2,497) -> C = 6 (22 clusters at once: 2.57 s per 35 PP-PC iterations against
+// 4.56 s at C = 1, 3.6 s at C = 7/8 where only 15 fit, 5.35 s with the block
+// engine).  The size depends on the context (d, max_batch) only, never on the
+// batch of one call, so a system's result is independent of how a batch is split.
+// The smaller C wins ties.  PPPC_CLUSTER=C forces a size.
 void cluster_geometry(ps_ctx* ctx) {
   if (ctx->cl_sized) return;
   ctx->cl_sized = true;
@@ -598,7 +605,8 @@ void cluster_geometry(ps_ctx* ctx) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int forced = std::getenv("PPPC_CLUSTER") ? std::atoi(std::getenv("PPPC_CLUSTER")) : 0;
-  int best_cover = 0;
+  const int batch = std::max(1, ctx->max_batch);
+  double best_score = 0.0;
   for (int C = 1; C <= kClusterMaxC; ++C) {
     if (forced > 0 && C != forced) continue;
     if (C > P.d) break;
@@ -606,8 +614,10 @@ void cluster_geometry(ps_ctx* ctx) {
     if (g.rows_max > syscluster_max_rows() || syscluster_smem(g) > static_cast<size_t>(smem_max)) continue;
     const int slots = syscluster_max_clusters(P.npe, P.ell_width, g);
     if (slots < 1) continue;
-    if (slots * C > best_cover) {
-      best_cover = slots * C;
+    const int waves = (batch + slots - 1) / slots;
+    const double score = static_cast<double>(C) * batch / waves;
+    if (score > best_score) {
+      best_score = score;
       ctx->cl_geo = g;
       ctx->cl_slots = slots;
     }
@@ -619,17 +629,17 @@ void cluster_geometry(ps_ctx* ctx) {
 }
 
 // Fine-propagation engine for a nonlinear element problem.
-//   block   (sysblock_kernel): one block per system, block barriers only; best
-//           when a system's seven vectors fit in one block's shared memory
-//           (configs[0], d = 2,497: fine sweep 9.8 -> 5.2 s per 35 PP-PC iterations);
-//   cluster (syscluster_kernel): one thread-block cluster per system, Krylov
-//           vectors in the cluster's shared memory / registers, hardware cluster
-//           barriers; for systems too large for one block whose vectors fit in a
-//           cluster (configs[1], d = 50,945);
+//   cluster (syscluster_kernel): one thread-block cluster of C CTAs per system,
+//           Krylov vectors in the cluster's shared memory, DSMEM halo exchange and
+//           sums; the default whenever the pattern qualifies (DevProblem::sb_ok) and
+//           some cluster size holds a CTA's working set on chip (configs[0],
+//           d = 2,497, C = 6; configs[1], d = 50,945, C = 9);
+//   block   (sysblock_kernel): one block per system, block barriers only, the
+//           seven vectors in one block's shared memory (small systems);
 //   lane    (propagate_kernel): one warp lane per system, groups of blocks with
 //           device-wide group barriers, vectors in HBM; any size (configs[3]/[4]).
 // ps_solver_settings.engine (1 lane, 2 block, 3 cluster) or PPPC_ENGINE=lane|sys|cluster
-// forces one; the pattern must qualify (DevProblem::sb_ok) for block and cluster.
+// forces one; the pattern must qualify for block and cluster.
 enum class Engine { Lane, Block, Cluster };
 Engine select_engine(ps_ctx* ctx, bool linear_path, bool probe_refill) {
   if (linear_path || probe_refill || !ctx->P.sb_ok) return Engine::Lane;
@@ -639,11 +649,10 @@ Engine select_engine(ps_ctx* ctx, bool linear_path, bool probe_refill) {
   const char* env = std::getenv("PPPC_ENGINE");
   if (e == 0 && env && std::strcmp(env, "lane") == 0) return Engine::Lane;
   if (e == 0 && env && std::strcmp(env, "sys") == 0) return Engine::Block;
-  const bool want_cluster = e == 3 || (env && std::strcmp(env, "cluster") == 0);
-  if (!want_cluster && sysblock_smem(ctx->P.d) <= kSbSmemMax) return Engine::Block;
   cluster_geometry(ctx);
   if (ctx->cl_geo.C > 0) return Engine::Cluster;
   if (e == 3) throw Failure(PS_ERR_BAD_ARG, "propagator: the cluster engine cannot hold this system on chip");
+  if (sysblock_smem(ctx->P.d) <= kSbSmemMax) return Engine::Block;
   return Engine::Lane;
 }
 
